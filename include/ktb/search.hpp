@@ -1,0 +1,71 @@
+// ktb/search.hpp -- search strategies (reference search.hpp): budget
+// arithmetic, the canonical-key evaluation cache with strict-< best (ties
+// keep the earliest), and the full / random / simulated-annealing / PSO
+// drivers with the reference's exact RNG consumption.
+#pragma once
+
+#include <cstdint>
+#include <functional>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "ktb/space.hpp"
+
+namespace ktb {
+
+using Evaluator = std::function<std::optional<double>(const Configuration&)>;
+
+enum class StrategyKind { full, random, annealing, pso };
+const char* to_string(StrategyKind k);
+StrategyKind strategy_kind_from(const std::string& name);
+
+struct StrategySpec {
+    StrategyKind kind = StrategyKind::full;
+    double fraction = 1.0;
+    double temperature = 4.0;
+    double alpha = 0.4;
+    double beta = 0.0;
+    double gamma = 0.4;
+    size_t swarm = 3;
+};
+
+struct TraceEntry {
+    size_t step = 0;
+    Configuration config;
+    std::optional<double> time_ms;
+    std::optional<double> best_so_far;
+};
+
+struct SearchOutcome {
+    std::optional<Configuration> best_config;
+    std::optional<double> best_time_ms;
+    std::vector<TraceEntry> trace;
+    size_t budget = 0;
+    size_t unique_evaluations = 0;
+    size_t failed_evaluations = 0;
+    size_t total_steps = 0;
+};
+
+size_t budget(unsigned long long valid_count, double fraction);
+double sa_acceptance(double t, double t_prime, double temperature);
+Configuration pso_move(const Configuration& x, const Configuration& p, const Configuration& g,
+                       double alpha, double beta, double gamma, const SearchSpace& space, Rng& rng);
+
+SearchOutcome run_full(const SearchSpace& space, const Evaluator& evaluate);
+SearchOutcome run_random(const SearchSpace& space, const Evaluator& evaluate, double fraction,
+                         uint64_t seed);
+SearchOutcome run_annealing(const SearchSpace& space, const Evaluator& evaluate,
+                            double temperature, double fraction, uint64_t seed);
+SearchOutcome run_pso(const SearchSpace& space, const Evaluator& evaluate, size_t swarm,
+                      double alpha, double beta, double gamma, double fraction, uint64_t seed);
+SearchOutcome run_search(const SearchSpace& space, const Evaluator& evaluate,
+                         const StrategySpec& strategy, uint64_t seed);
+
+// The unit list a sharded executor distributes: the enumeration indices a
+// full search visits (0..N-1) or the random search's sample, in visit order.
+// Only defined for the order-independent strategies (full, random).
+std::vector<uint64_t> planned_indices(const SearchSpace& space, const StrategySpec& strategy,
+                                      uint64_t seed, size_t* budget_out);
+
+}  // namespace ktb

@@ -1,0 +1,105 @@
+// ktb/space.hpp -- parameter spaces (reference space.hpp): parameters,
+// constraint expressions and native predicates; odometer enumeration (first
+// parameter slowest) cached and shared between copies; streaming counts;
+// uniform, unique and neighbour sampling with the reference's exact RNG
+// consumption, so seeded searches visit the same configurations.
+//
+// B200-side differences (same results): enumeration runs on all host cores
+// (the raw space is split on its leading parameters and the per-thread
+// results are concatenated in order) and is stored as one flat value table;
+// Configuration objects are materialized from it on demand.
+#pragma once
+
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "ktb/config.hpp"
+#include "ktb/constraint.hpp"
+#include "ktb/rng.hpp"
+
+namespace ktb {
+
+struct Parameter {
+    std::string name;
+    std::vector<Value> values;
+    std::vector<std::string> labels;
+    const std::string* label_of(Value v) const;
+};
+
+struct Predicate {
+    std::string label;
+    std::function<bool(const Configuration&)> fn;
+};
+
+class SearchSpace {
+  public:
+    static constexpr unsigned long long kEnumerationLimit = 10'000'000ull;
+
+    SearchSpace() = default;
+    SearchSpace(const SearchSpace& other);
+    SearchSpace& operator=(const SearchSpace& other);
+
+    SearchSpace& add_parameter(std::string name, std::vector<Value> values,
+                               std::vector<std::string> labels = {});
+    SearchSpace& add_constraint(std::string text);
+    SearchSpace& add_predicate(std::string label, std::function<bool(const Configuration&)> fn);
+    SearchSpace& add_predicate(Predicate p);
+
+    const std::vector<Parameter>& parameters() const { return params_; }
+    const std::vector<ConstraintExpr>& constraints() const { return constraints_; }
+    const std::vector<Predicate>& predicates() const { return predicates_; }
+    size_t parameter_index(std::string_view name) const;
+    const Parameter& parameter(std::string_view name) const;
+    bool has_parameter(std::string_view name) const;
+    const std::shared_ptr<const Configuration::Names>& names() const { return names_; }
+    unsigned long long raw_size() const;
+
+    bool satisfies(const Configuration& c) const;
+    bool is_valid(const Configuration& c) const;
+    Configuration make_configuration(std::vector<Value> values) const;
+
+    // All valid configurations, enumeration order (cached).
+    const std::vector<Configuration>& enumerate_valid() const;
+    // The same as a flat table: row i = values of configuration i (cached).
+    const std::vector<Value>& valid_table() const;
+    Configuration config_at(size_t index) const;
+    unsigned long long valid_count() const;
+    unsigned long long constraint_only_count() const;
+
+    Configuration random_valid(Rng& rng) const;
+    Configuration random_neighbor(const Configuration& c, Rng& rng) const;
+    std::vector<Configuration> sample_unique(size_t n, Rng& rng) const;
+    // Enumeration indices of sample_unique's draw (same RNG consumption);
+    // only for spaces within the enumeration limit.
+    std::vector<uint64_t> sample_unique_indices(size_t n, Rng& rng) const;
+
+  private:
+    static constexpr size_t kRejectionCap = 1'000'000;
+    struct Cache {
+        std::shared_ptr<const std::vector<Value>> table;
+        std::shared_ptr<const std::vector<Configuration>> configs;
+        std::optional<unsigned long long> count;
+    };
+    void rebuild_names();
+    void invalidate();
+    void require_parameters() const;
+    bool satisfies_values(const Value* v, Configuration& scratch) const;
+    // Enumerates valid rows (values) of the raw space; parallel over threads.
+    std::vector<Value> enumerate_table() const;
+    unsigned long long count_valid(bool predicates) const;
+    Configuration random_raw(Rng& rng) const;
+
+    std::vector<Parameter> params_;
+    std::shared_ptr<const Configuration::Names> names_;
+    std::vector<ConstraintExpr> constraints_;
+    std::vector<Predicate> predicates_;
+    mutable std::mutex mu_;
+    mutable Cache cache_;
+};
+
+}  // namespace ktb

@@ -1,0 +1,875 @@
+// backend.cpp -- ktc.h layer 2: ktune::Backend::evaluate on the B200.
+//
+// One evaluation: cubin from the NVRTC pool (compiled from the
+// family source with the configuration as -D defines) -> cuModuleLoadData ->
+// launch geometry from the request (grid = ceil(global/local), block =
+// local) -> output poisoned with NaN -> 1 warm-up + R timed launches (CUDA
+// events, L2 flushed before each) -> device verification of the output
+// against the bound reference -> ktc_result.
+//
+// Inputs are materialized from the request's recipes once per argument list
+// (std::mt19937_64, bit-identical to the reference), uploaded in the family's
+// device layout, and the family's device reference (builtin.cu, bit-identical
+// to the CPU oracle) is computed right after upload.
+#include <cuda.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "core.hpp"
+#include "ktb/arguments.hpp"
+#include "nvrtc_pool.hpp"
+
+namespace {
+
+#include "kernel_sources.inc"  // kConvSource, kGemmSource, kGemmTf32Source
+
+using namespace ktc;
+using Clock = std::chrono::steady_clock;
+
+double ms_since(Clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+enum Family { FAM_CONV, FAM_GEMM, FAM_GEMM_TF32, FAM_CUSTOM };
+
+size_t round_up(size_t v, size_t m) { return (v + m - 1) / m * m; }
+
+// Device-resident inputs, outputs and reference of one argument list.
+struct Inputs {
+    std::string sig;
+    Family fam = FAM_CUSTOM;
+    // conv
+    int X = 0, Y = 0, F = 0, ipitch = 0, rows = 0;
+    float W = 1.0f;
+    std::vector<float> taps;
+    // gemm
+    int M = 0, N = 0, K = 0;
+    float alpha = 1.0f, beta = 0.0f;
+    // all: device copy per argument (0 for scalars) and the argument list
+    std::vector<ktb::ArgumentSpec> args;
+    std::vector<CUdeviceptr> dev;
+    std::vector<size_t> bytes;
+    // outputs (in argument order): candidate buffer, reference buffer
+    std::vector<int> out_arg;
+    std::vector<CUdeviceptr> out, ref;
+    std::vector<size_t> out_count;
+    std::vector<int> out_type;
+    bool has_reference = false;
+    std::vector<std::string> ref_digest;  // lazily computed
+};
+
+struct Plan {
+    const std::string* src = nullptr;
+    std::string src_id;
+    std::vector<std::string> opts;
+    std::string entry;
+    unsigned grid[3] = {1, 1, 1}, block[3] = {1, 1, 1};
+    unsigned smem = 0;
+    int tma_mode = 0;  // 1: conv halo tile box (BW x BH)
+    unsigned box[2] = {0, 0};
+};
+
+std::string define(const char* name, long long v) {
+    return std::string("-D") + name + "=" + std::to_string(v);
+}
+
+}  // namespace
+
+struct ktc_backend {
+    ktc_ctx* ctx = nullptr;
+    ktc_backend_options opts{};
+    std::string name;
+    std::string cache_dir;
+    std::unique_ptr<Inputs> in;
+    std::map<std::string, std::string> custom_sources;  // path -> text
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Request helpers
+// ---------------------------------------------------------------------------
+
+struct ParamView {
+    const ktc_request* r;
+    bool get(const char* name, long long* v) const {
+        for (int i = 0; i < r->n_params; ++i)
+            if (std::strcmp(r->param_names[i], name) == 0) {
+                *v = r->param_values[i];
+                return true;
+            }
+        return false;
+    }
+};
+
+Family family_of(const char* name) {
+    std::string n = name ? name : "";
+    if (n == "conv") return FAM_CONV;
+    if (n == "gemm") return FAM_GEMM;
+    if (n == "gemm_tf32") return FAM_GEMM_TF32;
+    return FAM_CUSTOM;
+}
+
+std::string signature(const ktc_request* r) {
+    std::ostringstream s;
+    s << (r->kernel_name ? r->kernel_name : "") << '|' << (r->source_ref ? r->source_ref : "");
+    for (int i = 0; i < r->n_args; ++i) {
+        const ktc_arg& a = r->args[i];
+        s << '|' << a.role << ',' << a.type << ',' << a.length << ',';
+        s.precision(17);
+        s << a.value << ',' << (a.fill ? a.fill : "none");
+    }
+    return s.str();
+}
+
+ktb::ArgumentSpec to_spec(const ktc_arg& a) {
+    ktb::ArgumentSpec s;
+    s.role = a.role == KTC_ARG_INPUT ? ktb::ArgRole::input
+             : a.role == KTC_ARG_OUTPUT ? ktb::ArgRole::output
+                                        : ktb::ArgRole::scalar;
+    s.type = a.type == KTC_I32 ? ktb::ElementType::i32 : ktb::ElementType::f32;
+    s.length = a.length;
+    s.value = a.value;
+    s.fill = a.fill ? a.fill : "none";
+    return s;
+}
+
+void set_msg(ktc_result* out, const std::string& m) {
+    std::snprintf(out->message, sizeof(out->message), "%s", m.c_str());
+}
+
+void free_inputs(ktc_backend* be) {
+    if (!be->in) return;
+    const Driver& d = driver();
+    if (!be->ctx->sticky) {
+        d.cuCtxSetCurrent(be->ctx->cu);
+        for (CUdeviceptr p : be->in->dev)
+            if (p) d.cuMemFree(p);
+        for (CUdeviceptr p : be->in->out)
+            if (p) d.cuMemFree(p);
+        for (CUdeviceptr p : be->in->ref)
+            if (p) d.cuMemFree(p);
+    }
+    be->in.reset();
+}
+
+#define CK(call, what)                                               \
+    do {                                                             \
+        CUresult rc_ = (call);                                       \
+        if (rc_ != CUDA_SUCCESS) return fail_cu(be->ctx, rc_, what); \
+    } while (0)
+
+// Checks the documented case-study argument layout (the same layout the
+// reference's synthetic backend requires, backend.hpp:416-473).
+bool check_layout(const ktc_request* r, Family fam, std::string* why) {
+    auto scalar = [&](int i) { return i < r->n_args && r->args[i].role == KTC_ARG_SCALAR; };
+    auto f32buf = [&](int i, int role) {
+        return i < r->n_args && r->args[i].role == role && r->args[i].type == KTC_F32;
+    };
+    if (fam == FAM_CONV) {
+        if (r->n_args == 7 && scalar(0) && scalar(1) && scalar(2) && scalar(3) &&
+            f32buf(4, KTC_ARG_INPUT) && f32buf(5, KTC_ARG_INPUT) && f32buf(6, KTC_ARG_OUTPUT))
+            return true;
+        *why = "expected scalars X, Y, FILTER, W then f32 image, filter and output buffers";
+        return false;
+    }
+    if (r->n_args == 8 && scalar(0) && scalar(1) && scalar(2) && scalar(3) && scalar(4) &&
+        f32buf(5, KTC_ARG_INPUT) && f32buf(6, KTC_ARG_INPUT) && f32buf(7, KTC_ARG_OUTPUT))
+        return true;
+    *why = "expected scalars M, N, K, ALPHA, BETA then f32 A, B and C buffers";
+    return false;
+}
+
+// Materializes, uploads and (for the built-in families) computes the device
+// reference.  Throws nothing; returns a ktc.h code.
+int build_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
+    const Driver& d = driver();
+    ktc_ctx* ctx = be->ctx;
+    auto in = std::make_unique<Inputs>();
+    in->sig = signature(r);
+    in->fam = fam;
+    for (int i = 0; i < r->n_args; ++i) in->args.push_back(to_spec(r->args[i]));
+    in->dev.assign(in->args.size(), 0);
+    in->bytes.assign(in->args.size(), 0);
+    // Ownership: register buffers in `in` as soon as they exist so the
+    // error paths below release them via free_inputs.
+    be->in = std::move(in);
+    Inputs& I = *be->in;
+    auto alloc = [&](size_t bytes, CUdeviceptr* p) { return d.cuMemAlloc(p, bytes ? bytes : 4); };
+
+    if (fam == FAM_CONV) {
+        I.X = int(I.args[0].value);
+        I.Y = int(I.args[1].value);
+        I.F = int(I.args[2].value);
+        I.W = float(I.args[3].value);
+        if (I.X <= 0 || I.Y <= 0 || I.F < 1 || I.F % 2 == 0) {
+            set_error("convolution scalars out of range");
+            return KTC_ERR_INVALID;
+        }
+        const size_t px = size_t(I.X) + I.F - 1, py = size_t(I.Y) + I.F - 1;
+        if (I.args[4].length != px * py || I.args[5].length != size_t(I.F) * I.F ||
+            I.args[6].length != size_t(I.X) * I.Y) {
+            set_error("convolution input sizes do not match the problem dimensions");
+            return KTC_ERR_INVALID;
+        }
+        // HBM layout: padded image re-pitched to a 64-float (256 B) row pitch
+        // with slack for the largest tile (512 x 512) and vector over-reads,
+        // zero-filled; every tile load of every configuration stays in bounds
+        // and every row start is 16-byte aligned for float4 / TMA.
+        I.ipitch = int(round_up(round_up(size_t(I.X), 512) + I.F + 8, 64));
+        I.rows = int(round_up(size_t(I.Y), 512) + I.F + 32);
+        std::vector<float> img(px * py);
+        ktb::materialize_into(I.args[4], img.data());
+        I.taps.resize(size_t(I.F) * I.F);
+        ktb::materialize_into(I.args[5], I.taps.data());
+        I.bytes[4] = size_t(I.ipitch) * I.rows * 4;
+        CK(alloc(I.bytes[4], &I.dev[4]), "cuMemAlloc(image)");
+        CK(d.cuMemsetD32Async(I.dev[4], 0, I.bytes[4] / 4, ctx->stream), "cuMemset(image)");
+        CK(d.cuStreamSynchronize(ctx->stream), "cuStreamSynchronize");
+        int st = ktc_upload_pitched(ctx, I.dev[4], size_t(I.ipitch) * 4, img.data(), px * 4, px * 4,
+                                    py);
+        if (st) return st;
+        I.bytes[5] = I.taps.size() * 4;
+        CK(alloc(I.bytes[5], &I.dev[5]), "cuMemAlloc(taps)");
+        CK(d.cuMemcpyHtoD(I.dev[5], I.taps.data(), I.bytes[5]), "cuMemcpyHtoD(taps)");
+        I.out_arg = {6};
+    } else if (fam == FAM_GEMM || fam == FAM_GEMM_TF32) {
+        I.M = int(I.args[0].value);
+        I.N = int(I.args[1].value);
+        I.K = int(I.args[2].value);
+        I.alpha = float(I.args[3].value);
+        I.beta = float(I.args[4].value);
+        if (I.M <= 0 || I.N <= 0 || I.K <= 0) {
+            set_error("matrix dimensions must be positive");
+            return KTC_ERR_INVALID;
+        }
+        if (I.args[5].length != size_t(I.K) * I.M || I.args[6].length != size_t(I.K) * I.N ||
+            I.args[7].length != size_t(I.M) * I.N) {
+            set_error("matrix sizes do not match the problem dimensions");
+            return KTC_ERR_INVALID;
+        }
+        for (int a = 5; a <= 7; ++a) {  // A, B, C (C pristine: kernels write a separate output)
+            std::vector<float> h(I.args[a].length);
+            ktb::materialize_into(I.args[a], h.data());
+            I.bytes[a] = h.size() * 4;
+            CK(alloc(I.bytes[a], &I.dev[a]), "cuMemAlloc(matrix)");
+            CK(d.cuMemcpyHtoD(I.dev[a], h.data(), I.bytes[a]), "cuMemcpyHtoD(matrix)");
+        }
+        I.out_arg = {7};
+    } else {
+        for (size_t a = 0; a < I.args.size(); ++a) {
+            if (I.args[a].role == ktb::ArgRole::scalar) continue;
+            I.bytes[a] = I.args[a].length * 4;
+            CK(alloc(I.bytes[a], &I.dev[a]), "cuMemAlloc(argument)");
+            if (I.args[a].role == ktb::ArgRole::output) I.out_arg.push_back(int(a));
+        }
+    }
+    for (int a : I.out_arg) {
+        CUdeviceptr p = 0, q = 0;
+        CK(alloc(I.args[a].length * 4, &p), "cuMemAlloc(output)");
+        I.out.push_back(p);
+        I.ref.push_back(q);
+        I.out_count.push_back(I.args[a].length);
+        I.out_type.push_back(I.args[a].type == ktb::ElementType::i32 ? KTC_I32 : KTC_F32);
+    }
+    I.ref_digest.assign(I.out.size(), "");
+
+    // Device reference of the built-in families (bit-identical to the oracle).
+    if (fam == FAM_CONV) {
+        CK(alloc(I.out_count[0] * 4, &I.ref[0]), "cuMemAlloc(reference)");
+        int X = I.X, Y = I.Y, F = I.F, ip = I.ipitch;
+        float W = I.W;
+        CUdeviceptr img = I.dev[4], taps = I.dev[5], out = I.ref[0];
+        void* p[] = {&X, &Y, &F, &W, &img, &ip, &taps, &out};
+        CK(launch(ctx, ctx->fn_conv_ref, unsigned((X + 31) / 32), unsigned((Y + 7) / 8), 1, 32, 8, 1,
+                  0, p),
+           "conv reference launch");
+        CK(d.cuStreamSynchronize(ctx->stream), "conv reference");
+        I.has_reference = true;
+    } else if (fam == FAM_GEMM || fam == FAM_GEMM_TF32) {
+        CK(alloc(I.out_count[0] * 4, &I.ref[0]), "cuMemAlloc(reference)");
+        int M = I.M, N = I.N, K = I.K;
+        float al = I.alpha, bt = I.beta;
+        CUdeviceptr A = I.dev[5], B = I.dev[6], C = I.dev[7], out = I.ref[0];
+        void* p[] = {&M, &N, &K, &al, &bt, &A, &B, &C, &out};
+        CK(launch(ctx, ctx->fn_gemm_ref, unsigned((N + 31) / 32), unsigned((M + 31) / 32), 1, 32, 8,
+                  1, 0, p),
+           "gemm reference launch");
+        CK(d.cuStreamSynchronize(ctx->stream), "gemm reference");
+        I.has_reference = true;
+    }
+    return KTC_OK;
+}
+
+int ensure_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
+    if (be->ctx->sticky) {
+        free_inputs(be);
+        int st = ktc_reset(be->ctx);
+        if (st) return st;
+    }
+    std::string sig = signature(r);
+    if (be->in && be->in->sig == sig) return KTC_OK;
+    free_inputs(be);
+    int st = build_inputs(be, r, fam);
+    if (st) free_inputs(be);
+    return st;
+}
+
+// Upload per-evaluation initial contents of custom-kernel buffers (inputs
+// and outputs follow their fill recipes, exactly as the reference's
+// external runner would receive them).
+int refresh_custom_buffers(ktc_backend* be) {
+    Inputs& I = *be->in;
+    for (size_t a = 0; a < I.args.size(); ++a) {
+        if (I.args[a].role == ktb::ArgRole::scalar) continue;
+        std::vector<char> h(I.bytes[a]);
+        ktb::materialize_into(I.args[a], h.data());
+        CK(driver().cuMemcpyHtoD(I.dev[a], h.data(), h.size()), "cuMemcpyHtoD(argument)");
+    }
+    return KTC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Plans: configuration -> NVRTC source/defines + launch geometry.
+// Returns false with a message for configurations this device cannot run
+// (reported as runtime_error, like a launch failure).
+// ---------------------------------------------------------------------------
+
+bool plan_conv(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why) {
+    const Inputs& I = *be->in;
+    ParamView pv{r};
+    long long XWG, YWG, XWPT, YWPT, LOCAL, VW, PAD, UNR;
+    if (!pv.get("XWG", &XWG) || !pv.get("YWG", &YWG) || !pv.get("XWPT", &XWPT) ||
+        !pv.get("YWPT", &YWPT) || !pv.get("LOCAL", &LOCAL) || !pv.get("VW", &VW) ||
+        !pv.get("PAD", &PAD) || !pv.get("UNR", &UNR)) {
+        *why = "the conv family needs XWG, YWG, XWPT, YWPT, LOCAL, VW, PAD, UNR";
+        return false;
+    }
+    auto pow2 = [](long long v) { return v > 0 && (v & (v - 1)) == 0; };
+    if (!pow2(XWG) || !pow2(YWG) || !pow2(XWPT) || !pow2(YWPT) || !(VW == 1 || VW == 2 || VW == 4 || VW == 8) ||
+        XWPT % VW != 0 || LOCAL < 0 || LOCAL > 2 || XWG * XWPT < 8 || XWG * XWPT > 512 ||
+        YWG * YWPT > 512) {
+        *why = "conv configuration outside the family's parameter domain";
+        return false;
+    }
+    const long long H = (I.F - 1) / 2, TX = XWG * XWPT, TY = YWG * YWPT;
+    p->src = &kConvSource;
+    p->src_id = "conv.cu#" + std::to_string(std::hash<std::string>()(kConvSource));
+    p->entry = "conv2d";
+    auto& o = p->opts;
+    o = {define("FS", I.F), define("XWG", XWG), define("YWG", YWG), define("XWPT", XWPT),
+         define("YWPT", YWPT), define("LOCAL", LOCAL), define("VW", VW),
+         define("PAD", LOCAL >= 1 ? PAD : 0), define("UNR", UNR ? 1 : 0),
+         define("GUARD", (I.X % TX != 0 || I.Y % TY != 0) ? 1 : 0),
+         define("OUT_VEC", I.X % VW == 0 ? 1 : 0)};
+    size_t smem_floats = 0;
+    if (LOCAL == 1) {
+        const long long SP = TX + 2 * H + PAD;
+        o.push_back(define("SP", SP));
+        smem_floats = size_t(SP * (TY + 2 * H) + 8);
+    } else if (LOCAL == 2) {
+        const long long PWO = std::min<long long>(TX, 128);
+        const long long BW = (PWO + 2 * H + 3) / 4 * 4 + 4 * PAD;
+        const long long TR = TY + 2 * H;
+        const long long NB = (TR + 255) / 256;
+        const long long BH = ((TR + NB - 1) / NB + 7) / 8 * 8;
+        const long long NP = TX / PWO;
+        const long long PF = BW * NB * BH;
+        o.insert(o.end(), {define("PWO", PWO), define("BW", BW), define("BH", BH),
+                           define("NB", NB), define("NP", NP), define("PF", PF)});
+        smem_floats = size_t(NP * PF + 4);
+        p->tma_mode = 1;
+        p->box[0] = unsigned(BW);
+        p->box[1] = unsigned(BH);
+    }
+    p->smem = unsigned(smem_floats * 4);
+    if (p->smem > be->ctx->limits.smem_per_block_optin) {
+        *why = "needs " + std::to_string(p->smem) + " bytes of shared memory; the device allows " +
+               std::to_string(be->ctx->limits.smem_per_block_optin);
+        return false;
+    }
+    if (r->ndim != 2 || r->local[0] != size_t(XWG) || r->local[1] != size_t(YWG)) {
+        *why = "request local size does not match (XWG, YWG)";
+        return false;
+    }
+    for (int k = 0; k < 2; ++k) {
+        p->block[k] = unsigned(r->local[k]);
+        p->grid[k] = unsigned((r->global[k] + r->local[k] - 1) / r->local[k]);
+    }
+    // The grid must cover the image (global = (X/XWPT, Y/YWPT) per the
+    // reference's modifiers, landscapes.hpp:87-92).
+    if ((long long)p->grid[0] * TX < I.X || (long long)p->grid[1] * TY < I.Y) {
+        *why = "request global size does not cover the image";
+        return false;
+    }
+    return true;
+}
+
+bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why) {
+    const Inputs& I = *be->in;
+    ParamView pv{r};
+    static const char* names[] = {"MWG", "NWG",  "KWG",  "MDIMC", "NDIMC", "SA",  "SB",
+                                  "MDIMA", "NDIMB", "STRM", "STRN", "VWM",  "VWN", "KWI"};
+    long long v[14];
+    for (int i = 0; i < 14; ++i)
+        if (!pv.get(names[i], &v[i])) {
+            *why = std::string("the gemm family needs parameter ") + names[i];
+            return false;
+        }
+    const long long MWG = v[0], NWG = v[1], KWG = v[2], MDIMC = v[3], NDIMC = v[4], SA = v[5],
+                    SB = v[6], KWI = v[13], VWM = v[11], VWN = v[12];
+    long long MDIMA = v[7], NDIMB = v[8];
+    auto pow2 = [](long long x) { return x > 0 && (x & (x - 1)) == 0; };
+    for (int i = 0; i < 14; ++i)
+        if (i != 5 && i != 6 && i != 9 && i != 10 && !pow2(v[i])) {
+            *why = "gemm configuration outside the family's parameter domain";
+            return false;
+        }
+    if (MWG % MDIMC || NWG % NDIMC || (MWG / MDIMC) % VWM || (NWG / NDIMC) % VWN || KWG % KWI ||
+        VWM > 8 || VWN > 8 || (MDIMC * NDIMC) % MDIMA || (MDIMC * NDIMC) % NDIMB ||
+        KWG % ((MDIMC * NDIMC) / MDIMA) || KWG % ((MDIMC * NDIMC) / NDIMB)) {
+        *why = "gemm configuration violates the family's divisibility rules";
+        return false;
+    }
+    if (I.M % MWG || I.N % NWG || I.K % KWG) {
+        *why = "problem size (" + std::to_string(I.M) + "x" + std::to_string(I.N) + "x" +
+               std::to_string(I.K) + ") is not a multiple of the (MWG, NWG, KWG) tile";
+        return false;
+    }
+    // Code identity: MDIMA / NDIMB only shape the shared-memory copies, so
+    // with SA = 0 / SB = 0 they are normalised away and those rows share one
+    // cubin (they are still timed as separate rows).
+    if (!SA) MDIMA = 8;
+    if (!SB) NDIMB = 8;
+    p->src = &kGemmSource;
+    p->src_id = "gemm.cu#" + std::to_string(std::hash<std::string>()(kGemmSource));
+    p->entry = "gemm";
+    p->opts = {define("MWG", MWG),     define("NWG", NWG),     define("KWG", KWG),
+               define("MDIMC", MDIMC), define("NDIMC", NDIMC), define("SA", SA ? 1 : 0),
+               define("SB", SB ? 1 : 0), define("MDIMA", MDIMA), define("NDIMB", NDIMB),
+               define("STRM", v[9] ? 1 : 0), define("STRN", v[10] ? 1 : 0), define("VWM", VWM),
+               define("VWN", VWN), define("KWI", KWI)};
+    p->smem = unsigned((SA * KWG * MWG + SB * KWG * NWG) * 4);
+    if (p->smem > be->ctx->limits.smem_per_block_optin) {
+        *why = "needs " + std::to_string(p->smem) + " bytes of shared memory";
+        return false;
+    }
+    if (r->ndim != 2 || r->local[0] != size_t(MDIMC) || r->local[1] != size_t(NDIMC)) {
+        *why = "request local size does not match (MDIMC, NDIMC)";
+        return false;
+    }
+    p->block[0] = unsigned(MDIMC);
+    p->block[1] = unsigned(NDIMC);
+    p->grid[0] = unsigned(I.M / MWG);
+    p->grid[1] = unsigned(I.N / NWG);
+    // global = (M*MDIMC/MWG, N*NDIMC/NWG) (landscapes.hpp:260-267)
+    if (r->global[0] != size_t(p->grid[0]) * MDIMC || r->global[1] != size_t(p->grid[1]) * NDIMC) {
+        *why = "request global size does not match the (MWG, NWG) tiling";
+        return false;
+    }
+    return true;
+}
+
+bool plan_gemm_tf32(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why);
+
+bool plan_custom(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why) {
+    const std::string path = r->source_ref ? r->source_ref : "";
+    auto it = be->custom_sources.find(path);
+    if (it == be->custom_sources.end()) {
+        std::ifstream f(path, std::ios::binary);
+        if (!f) {
+            *why = "cannot read kernel source \"" + path + "\"";
+            return false;
+        }
+        std::ostringstream s;
+        s << f.rdbuf();
+        it = be->custom_sources.emplace(path, s.str()).first;
+    }
+    p->src = &it->second;
+    p->src_id = path + "#" + std::to_string(std::hash<std::string>()(it->second));
+    p->entry = r->kernel_name;
+    for (int i = 0; i < r->n_params; ++i)
+        p->opts.push_back(define(r->param_names[i], r->param_values[i]));
+    if (r->ndim < 1 || r->ndim > 3) {
+        *why = "thread sizes must have 1 to 3 dimensions";
+        return false;
+    }
+    for (int k = 0; k < r->ndim; ++k) {
+        if (r->local[k] == 0) {
+            *why = "zero local size";
+            return false;
+        }
+        p->block[k] = unsigned(r->local[k]);
+        p->grid[k] = unsigned((r->global[k] + r->local[k] - 1) / r->local[k]);
+    }
+    return true;
+}
+
+}  // namespace
+
+// gemm_tf32.cpp provides the tcgen05 family plan and its launch.
+namespace ktc {
+bool plan_tf32(ktc_ctx* ctx, int M, int N, int K, const ktc_request* r, std::string* src_id,
+               const std::string** src, std::vector<std::string>* opts, std::string* entry,
+               unsigned grid[3], unsigned block[3], unsigned* smem, std::string* why);
+}
+
+namespace {
+
+bool plan_gemm_tf32(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why) {
+    const Inputs& I = *be->in;
+    return ktc::plan_tf32(be->ctx, I.M, I.N, I.K, r, &p->src_id, &p->src, &p->opts, &p->entry,
+                          p->grid, p->block, &p->smem, why);
+}
+
+int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
+    std::memset(out, 0, sizeof(*out));
+    out->status = KTC_STATUS_RUNTIME_ERROR;
+    out->verification = KTC_VERIFY_SKIPPED;
+    const Driver& d = driver();
+    ktc_ctx* ctx = be->ctx;
+    const Family fam = family_of(r->kernel_name);
+    std::string why;
+    if (fam != FAM_CUSTOM && !check_layout(r, fam, &why)) {
+        set_msg(out, "runtime_error: " + why);
+        return KTC_OK;
+    }
+    int st = make_current(ctx);
+    if (st) return st;
+    st = ensure_inputs(be, r, fam);
+    if (st) return st;
+    Inputs& I = *be->in;
+
+    Plan plan;
+    bool ok = fam == FAM_CONV   ? plan_conv(be, r, &plan, &why)
+              : fam == FAM_GEMM ? plan_gemm(be, r, &plan, &why)
+              : fam == FAM_GEMM_TF32 ? plan_gemm_tf32(be, r, &plan, &why)
+                                     : plan_custom(be, r, &plan, &why);
+    if (!ok) {
+        set_msg(out, why);
+        return KTC_OK;
+    }
+
+    // 1. cubin
+    auto t0 = Clock::now();
+    bool hit = false;
+    CubinPtr cubin = CompileService::instance().get(plan.src_id, *plan.src, plan.opts, &hit);
+    out->compile_ms = hit ? 0.0 : ms_since(t0);
+    out->compile_cache_hit = hit ? 1 : 0;
+    if (!cubin->ok()) {
+        out->status = KTC_STATUS_COMPILE_ERROR;
+        set_msg(out, "NVRTC: " + cubin->log.substr(0, 480));
+        return KTC_OK;
+    }
+
+    // 2. module
+    t0 = Clock::now();
+    ktc_fn* fn = nullptr;
+    st = ktc_load(ctx, cubin->image.data(), cubin->image.size(), plan.entry.c_str(), &fn);
+    if (st) {
+        set_msg(out, last_error());
+        return ctx->sticky ? st : KTC_OK;
+    }
+    struct Unload {
+        ktc_fn* f;
+        ~Unload() { ktc_unload(f); }
+    } unload{fn};
+
+    alignas(64) CUtensorMap tmap;
+    std::memset(&tmap, 0, sizeof(tmap));
+    std::vector<void*> params;
+    // Scalar storage must outlive the launches.
+    int iX = 0, iY = 0, iP = 0, iM = 0, iN = 0, iK = 0;
+    float fW = 0, fA = 0, fB = 0;
+    CUdeviceptr pImg = 0, pOut = 0, pA = 0, pB = 0, pC = 0;
+    std::vector<long long> scal_i;  // custom scalars
+    std::vector<float> scal_f;
+    std::vector<CUdeviceptr> ptrs;
+    if (fam == FAM_CONV) {
+        if (ktc_set_symbol(fn, "c_taps", I.taps.data(), I.taps.size() * 4) != KTC_OK) {
+            set_msg(out, last_error());
+            return ctx->sticky ? KTC_ERR_LAUNCH : KTC_OK;
+        }
+        if (plan.tma_mode == 1) {
+            cuuint64_t dims[2] = {cuuint64_t(I.ipitch), cuuint64_t(I.rows)};
+            cuuint64_t strides[1] = {cuuint64_t(I.ipitch) * 4};
+            cuuint32_t box[2] = {plan.box[0], plan.box[1]};
+            cuuint32_t estr[2] = {1, 1};
+            CUresult rc = d.cuTensorMapEncodeTiled(
+                &tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, reinterpret_cast<void*>(I.dev[4]), dims,
+                strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (rc != CUDA_SUCCESS) {
+                set_msg(out, cu_error_text(rc, "cuTensorMapEncodeTiled"));
+                return KTC_OK;
+            }
+        }
+        iX = I.X;
+        iY = I.Y;
+        fW = I.W;
+        pImg = I.dev[4];
+        iP = I.ipitch;
+        pOut = I.out[0];
+        params = {&iX, &iY, &fW, &pImg, &iP, &pOut, &tmap};
+    } else if (fam == FAM_GEMM || fam == FAM_GEMM_TF32) {
+        iM = I.M;
+        iN = I.N;
+        iK = I.K;
+        fA = I.alpha;
+        fB = I.beta;
+        pA = I.dev[5];
+        pB = I.dev[6];
+        pC = I.dev[7];
+        pOut = I.out[0];
+        params = {&iM, &iN, &iK, &fA, &fB, &pA, &pB, &pC, &pOut};
+    } else {
+        st = refresh_custom_buffers(be);
+        if (st) return st;
+        scal_i.resize(I.args.size());
+        scal_f.resize(I.args.size());
+        ptrs.resize(I.args.size());
+        size_t oi = 0;
+        for (size_t a = 0; a < I.args.size(); ++a) {
+            const auto& s = I.args[a];
+            if (s.role == ktb::ArgRole::scalar) {
+                if (s.type == ktb::ElementType::i32) {
+                    scal_i[a] = (long long)(int)s.value;
+                    params.push_back(&scal_i[a]);  // little-endian: low 4 bytes = int
+                } else {
+                    scal_f[a] = float(s.value);
+                    params.push_back(&scal_f[a]);
+                }
+            } else if (s.role == ktb::ArgRole::output) {
+                ptrs[a] = I.out[oi++];
+                params.push_back(&ptrs[a]);
+            } else {
+                ptrs[a] = I.dev[a];
+                params.push_back(&ptrs[a]);
+            }
+        }
+        // outputs start from their recipe contents
+        for (size_t k = 0; k < I.out_arg.size(); ++k) {
+            CUresult rc = d.cuMemcpyDtoDAsync(I.out[k], I.dev[I.out_arg[k]],
+                                              I.out_count[k] * 4, ctx->stream);
+            if (rc != CUDA_SUCCESS) return fail_cu(ctx, rc, "cuMemcpyDtoD(output init)");
+        }
+    }
+    out->load_ms = ms_since(t0);
+
+    // 3. run: outputs poisoned with NaN so a configuration that skips
+    // elements can never pass on a previous configuration's results.
+    t0 = Clock::now();
+    if (fam != FAM_CUSTOM) {
+        for (size_t k = 0; k < I.out.size(); ++k) {
+            CUresult rc = d.cuMemsetD32Async(I.out[k], 0xFFFFFFFFu, I.out_count[k], ctx->stream);
+            if (rc != CUDA_SUCCESS) return fail_cu(ctx, rc, "cuMemsetD32(output)");
+        }
+    }
+    const long long launches0 = ctx->launches;
+    float best = 0.0f;
+    const int reps = r->repetitions > 0 ? r->repetitions : 1;
+    st = ktc_launch_timed(ctx, fn, plan.grid, plan.block, plan.smem, params.data(),
+                          be->opts.warmup, reps, be->opts.flush_l2, &best, nullptr);
+    out->run_ms = ms_since(t0);
+    if (st) {
+        set_msg(out, last_error());
+        out->kernel_launches = int(ctx->launches - launches0);
+        // Sticky faults poison the context: reset now so the next
+        // configuration starts clean (inputs are rebuilt lazily).
+        if (ctx->sticky) {
+            unload.f = nullptr;
+            delete fn;  // module died with the context
+            free_inputs(be);
+            int rs = ktc_reset(ctx);
+            if (rs) return rs;
+        }
+        return KTC_OK;
+    }
+    if (!(best > 0.0f) || !std::isfinite(best)) {
+        set_msg(out, "non-positive kernel time");
+        return KTC_OK;
+    }
+    out->status = KTC_STATUS_SUCCESS;
+    out->time_ms = double(best);
+    out->n_outputs = int(I.out.size());
+
+    // 4. verification on the device
+    t0 = Clock::now();
+    if (be->opts.verify && r->want_outputs && I.has_reference) {
+        ktc_verify_report total{};
+        total.pass = 1;
+        for (size_t k = 0; k < I.out.size(); ++k) {
+            ktc_verify_report rep;
+            bool nan_abs = false, nan_rel = false;
+            st = verify_pair(ctx, I.out[k], I.ref[k], I.out_count[k], I.out_type[k],
+                             be->opts.rel_tol, be->opts.abs_tol, &rep, &nan_abs, &nan_rel);
+            if (st) return st;
+            merge_reports(&total, rep, nan_abs, nan_rel, k);
+        }
+        out->report = total;
+        out->verification = total.pass ? KTC_VERIFY_PASS : KTC_VERIFY_FAIL;
+    }
+    out->verify_ms = ms_since(t0);
+
+    // 5. digests (adapter use: the reference tuner's digest comparison)
+    if (be->opts.digest_outputs) {
+        for (size_t k = 0; k < I.out.size() && k < KTC_MAX_OUTPUTS; ++k) {
+            std::vector<uint32_t> h(I.out_count[k]);
+            st = ktc_download(ctx, h.data(), I.out[k], h.size() * 4);
+            if (st) return st;
+            ktc_digest_hex(ktc_digest_words(h.data(), h.size()), out->output_digests[k]);
+        }
+    }
+    out->kernel_launches = int(ctx->launches - launches0);
+    return KTC_OK;
+}
+
+}  // namespace
+
+using namespace ktc;
+
+extern "C" {
+
+void ktc_backend_default_options(ktc_backend_options* o) {
+    std::memset(o, 0, sizeof(*o));
+    o->warmup = 1;
+    o->flush_l2 = 1;
+    o->verify = 1;
+    o->rel_tol = 1e-4;
+    o->abs_tol = 1e-6;
+    o->compile_threads = 0;
+    o->cache_dir = nullptr;
+    o->digest_outputs = 0;
+}
+
+int ktc_backend_open(int ordinal, const ktc_backend_options* opts, ktc_backend** out) {
+    *out = nullptr;
+    ktc_ctx* ctx = nullptr;
+    int st = ktc_open(ordinal, &ctx);
+    if (st) return st;
+    auto* be = new ktc_backend;
+    be->ctx = ctx;
+    if (opts) be->opts = *opts;
+    else ktc_backend_default_options(&be->opts);
+    if (be->opts.cache_dir) be->cache_dir = be->opts.cache_dir;
+    be->opts.cache_dir = nullptr;
+    CompileService::instance().configure(be->opts.compile_threads, be->cache_dir);
+    be->name = std::string("cuda:sm_100a:") + ctx->limits.name;
+    *out = be;
+    return KTC_OK;
+}
+
+void ktc_backend_close(ktc_backend* be) {
+    if (!be) return;
+    free_inputs(be);
+    ktc_close(be->ctx);
+    delete be;
+}
+
+const char* ktc_backend_name(ktc_backend* be) { return be ? be->name.c_str() : ""; }
+ktc_ctx* ktc_backend_ctx(ktc_backend* be) { return be ? be->ctx : nullptr; }
+
+int ktc_backend_evaluate(ktc_backend* be, const ktc_request* req, ktc_result* out) {
+    if (!be || !req || !out) return KTC_ERR_INVALID;
+    try {
+        return evaluate(be, req, out);
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return KTC_ERR_INVALID;
+    }
+}
+
+int ktc_backend_prefetch(ktc_backend* be, const ktc_request* req) {
+    if (!be || !req) return KTC_ERR_INVALID;
+    try {
+        const Family fam = family_of(req->kernel_name);
+        std::string why;
+        if (fam != FAM_CUSTOM && !check_layout(req, fam, &why)) return KTC_OK;
+        // Plans need the problem scalars only; build a light Inputs view.
+        if (!be->in || be->in->sig != signature(req)) {
+            int st = make_current(be->ctx);
+            if (st) return st;
+            st = ensure_inputs(be, req, fam);
+            if (st) return st;
+        }
+        Plan plan;
+        bool ok = fam == FAM_CONV   ? plan_conv(be, req, &plan, &why)
+                  : fam == FAM_GEMM ? plan_gemm(be, req, &plan, &why)
+                  : fam == FAM_GEMM_TF32 ? plan_gemm_tf32(be, req, &plan, &why)
+                                         : plan_custom(be, req, &plan, &why);
+        if (ok) CompileService::instance().prefetch(plan.src_id, *plan.src, plan.opts);
+        return KTC_OK;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return KTC_ERR_INVALID;
+    }
+}
+
+int ktc_backend_set_reference(ktc_backend* be, const ktc_request* req, int n_buffers,
+                              const void* const* buffers, const size_t* lengths, const int* types) {
+    if (!be || !req) return KTC_ERR_INVALID;
+    int st = make_current(be->ctx);
+    if (st) return st;
+    const Family fam = family_of(req->kernel_name);
+    st = ensure_inputs(be, req, fam);
+    if (st) return st;
+    Inputs& I = *be->in;
+    if (n_buffers != int(I.out.size())) {
+        set_error("reference has " + std::to_string(n_buffers) + " buffers, kernel has " +
+                  std::to_string(I.out.size()) + " outputs");
+        return KTC_ERR_INVALID;
+    }
+    const Driver& d = driver();
+    for (int k = 0; k < n_buffers; ++k) {
+        if (lengths[k] != I.out_count[k] || types[k] != I.out_type[k]) {
+            set_error("reference buffer " + std::to_string(k) + " differs in length or type");
+            return KTC_ERR_INVALID;
+        }
+        if (!I.ref[k]) {
+            CUresult rc = d.cuMemAlloc(&I.ref[k], lengths[k] * 4);
+            if (rc != CUDA_SUCCESS) return fail_cu(be->ctx, rc, "cuMemAlloc(reference)");
+        }
+        CUresult rc = d.cuMemcpyHtoD(I.ref[k], buffers[k], lengths[k] * 4);
+        if (rc != CUDA_SUCCESS) return fail_cu(be->ctx, rc, "cuMemcpyHtoD(reference)");
+        I.ref_digest[k].clear();
+    }
+    I.has_reference = true;
+    return KTC_OK;
+}
+
+int ktc_backend_read_output(ktc_backend* be, int index, void* dst, size_t bytes) {
+    if (!be || !be->in || index < 0 || index >= int(be->in->out.size())) return KTC_ERR_INVALID;
+    size_t n = std::min(bytes, be->in->out_count[index] * 4);
+    return ktc_download(be->ctx, dst, be->in->out[index], n);
+}
+
+int ktc_backend_read_reference(ktc_backend* be, const ktc_request* req, int index, void* dst,
+                               size_t bytes, char digest_hex[17]) {
+    if (!be || !req) return KTC_ERR_INVALID;
+    int st = make_current(be->ctx);
+    if (st) return st;
+    st = ensure_inputs(be, req, family_of(req->kernel_name));
+    if (st) return st;
+    Inputs& I = *be->in;
+    if (index < 0 || index >= int(I.out.size()) || !I.ref[index]) {
+        set_error("no reference output " + std::to_string(index));
+        return KTC_ERR_INVALID;
+    }
+    std::vector<uint32_t> h(I.out_count[index]);
+    st = ktc_download(be->ctx, h.data(), I.ref[index], h.size() * 4);
+    if (st) return st;
+    if (dst) std::memcpy(dst, h.data(), std::min(bytes, h.size() * 4));
+    if (digest_hex) ktc_digest_hex(ktc_digest_words(h.data(), h.size()), digest_hex);
+    return KTC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,261 @@
+// builtin.cu -- fixed (non-tuned) device kernels of the B200 evaluation
+// backend, compiled ahead of time by nvcc for sm_100a and embedded in
+// libktc.so as a cubin:
+//
+//   ktc_conv_reference / ktc_gemm_reference
+//       The device-side reference ("SetReference" in CLTune terms).  They
+//       perform exactly the reference oracle's per-element operation
+//       sequence -- rounded fp32 multiply, then rounded fp32 add, in the
+//       oracle's loop order (landscapes.hpp:129-140 and :301-309) -- so their
+//       output is BIT-IDENTICAL to conv_apply/gemm_apply on the CPU
+//       (tests/test_gpu_parity.py checks the FNV digests against the
+//       reference's golden digests).  Compiled with -fmad=false and explicit
+//       __fmul_rn/__fadd_rn so no FMA contraction can creep in.
+//
+//   ktc_verify_partial / ktc_verify_final / ktc_verify_after
+//       The device-side output verification that replaces the host loop of
+//       verify_outputs (tuner.hpp:39-106).  Same pass rule (in double),
+//       same report fields, same first-failure / first-argmax indices, and
+//       the reference's NaN quirk (a NaN error resets the running maximum)
+//       reproduced exactly via a second pass over the suffix after the last
+//       NaN.
+//
+//   ktc_l2_flush
+//       Streams a buffer larger than L2 through the cache between timed
+//       repetitions (read-only, so no write-back lands inside the next
+//       timed kernel).
+#include <stdint.h>
+
+#define KTC_VERIFY_THREADS 256
+
+// ---------------------------------------------------------------------------
+// Device reference: convolution.  One thread per output; image is the
+// re-pitched padded image (row pitch `ipitch` floats).
+// ---------------------------------------------------------------------------
+extern "C" __global__ void ktc_conv_reference(int X, int Y, int F, float W,
+                                              const float* __restrict__ img, int ipitch,
+                                              const float* __restrict__ taps,
+                                              float* __restrict__ out) {
+    const int col = blockIdx.x * blockDim.x + threadIdx.x;
+    const int row = blockIdx.y * blockDim.y + threadIdx.y;
+    if (col >= X || row >= Y) return;
+    float acc = 0.0f;
+    for (int j = 0; j < F; ++j) {
+        const float* line = img + (size_t)(row + j) * ipitch + col;
+        const float* tap = taps + j * F;
+        for (int i = 0; i < F; ++i) acc = __fadd_rn(acc, __fmul_rn(tap[i], line[i]));
+    }
+    out[(size_t)row * X + col] = __fmul_rn(W, acc);
+}
+
+// ---------------------------------------------------------------------------
+// Device reference: C = alpha * A^T B + beta * C.  Shared-memory tiled, but
+// each thread owns one output and adds the products in ascending k with
+// separate rounding -- the oracle's exact sequence.
+// ---------------------------------------------------------------------------
+#define RT 32
+extern "C" __global__ void __launch_bounds__(RT * 8)
+ktc_gemm_reference(int M, int N, int K, float alpha, float beta,
+                   const float* __restrict__ A, const float* __restrict__ B,
+                   const float* __restrict__ C, float* __restrict__ out) {
+    __shared__ float As[RT][RT + 1];  // [k][m]
+    __shared__ float Bs[RT][RT + 1];  // [k][n]
+    const int tx = threadIdx.x;       // n within tile (0..31)
+    const int ty = threadIdx.y;       // 0..7, each owns 4 rows
+    const int m0 = blockIdx.y * RT, n0 = blockIdx.x * RT;
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    for (int k0 = 0; k0 < K; k0 += RT) {
+        for (int r = ty; r < RT; r += 8) {
+            const int k = k0 + r;
+            As[r][tx] = (k < K && m0 + tx < M) ? A[(size_t)k * M + m0 + tx] : 0.0f;
+            Bs[r][tx] = (k < K && n0 + tx < N) ? B[(size_t)k * N + n0 + tx] : 0.0f;
+        }
+        __syncthreads();
+        const int kmax = min(RT, K - k0);
+        for (int kk = 0; kk < kmax; ++kk) {
+            const float b = Bs[kk][tx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = __fadd_rn(acc[q], __fmul_rn(As[kk][ty * 4 + q], b));
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int m = m0 + ty * 4 + q, n = n0 + tx;
+        if (m < M && n < N) {
+            const size_t idx = (size_t)m * N + n;
+            out[idx] = __fadd_rn(__fmul_rn(alpha, acc[q]), __fmul_rn(beta, C[idx]));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Verification.  Partial state per thread/block:
+//   first_fail   lowest index failing the pass rule (UINT64_MAX if none)
+//   max_abs      max |c-r| over non-NaN errors, argmax = lowest index of it
+//   nan_abs      highest index whose |c-r| is NaN (-1 if none)
+//   max_rel      max rel error over non-NaN rel errors
+//   nan_rel      highest index whose rel error is NaN (-1 if none)
+// ---------------------------------------------------------------------------
+struct VerifyPartial {
+    unsigned long long first_fail;
+    unsigned long long argmax;
+    long long nan_abs;
+    long long nan_rel;
+    double max_abs;
+    double max_rel;
+};
+
+__device__ __forceinline__ void vp_init(VerifyPartial& p) {
+    p.first_fail = ~0ull;
+    p.argmax = ~0ull;
+    p.nan_abs = -1;
+    p.nan_rel = -1;
+    p.max_abs = -1.0;
+    p.max_rel = -1.0;
+}
+
+__device__ __forceinline__ void vp_merge(VerifyPartial& a, const VerifyPartial& b) {
+    a.first_fail = a.first_fail < b.first_fail ? a.first_fail : b.first_fail;
+    if (b.max_abs > a.max_abs || (b.max_abs == a.max_abs && b.argmax < a.argmax)) {
+        a.max_abs = b.max_abs;
+        a.argmax = b.argmax;
+    }
+    a.nan_abs = a.nan_abs > b.nan_abs ? a.nan_abs : b.nan_abs;
+    a.nan_rel = a.nan_rel > b.nan_rel ? a.nan_rel : b.nan_rel;
+    a.max_rel = a.max_rel > b.max_rel ? a.max_rel : b.max_rel;
+}
+
+__device__ __forceinline__ void vp_shfl_merge(VerifyPartial& p, int offset) {
+    VerifyPartial o;
+    o.first_fail = __shfl_down_sync(0xffffffffu, p.first_fail, offset);
+    o.argmax = __shfl_down_sync(0xffffffffu, p.argmax, offset);
+    o.nan_abs = __shfl_down_sync(0xffffffffu, p.nan_abs, offset);
+    o.nan_rel = __shfl_down_sync(0xffffffffu, p.nan_rel, offset);
+    o.max_abs = __shfl_down_sync(0xffffffffu, p.max_abs, offset);
+    o.max_rel = __shfl_down_sync(0xffffffffu, p.max_rel, offset);
+    vp_merge(p, o);
+}
+
+__device__ __forceinline__ void vp_block_reduce(VerifyPartial& p, VerifyPartial* out) {
+    __shared__ VerifyPartial warp_part[KTC_VERIFY_THREADS / 32];
+    for (int off = 16; off > 0; off >>= 1) vp_shfl_merge(p, off);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) warp_part[warp] = p;
+    __syncthreads();
+    if (warp == 0) {
+        if (lane < KTC_VERIFY_THREADS / 32) p = warp_part[lane];
+        else vp_init(p);
+        for (int off = 16; off > 0; off >>= 1) vp_shfl_merge(p, off);
+        if (lane == 0) *out = p;
+    }
+}
+
+template <bool IS_F32>
+__device__ __forceinline__ void vp_element(VerifyPartial& p, unsigned long long i, double c,
+                                           double r, double rel_tol, double abs_tol, bool equal) {
+    const double abs_err = fabs(c - r);
+    double rel_err;
+    bool ok;
+    if (IS_F32) {
+        const double mag = fabs(r);
+        rel_err = mag > 0.0 ? abs_err / mag : 0.0;
+        ok = abs_err <= abs_tol + rel_tol * mag;  // false for NaN
+    } else {
+        rel_err = abs_err;
+        ok = equal;
+    }
+    if (!ok && i < p.first_fail) p.first_fail = i;
+    if (abs_err != abs_err) {
+        p.nan_abs = (long long)i;  // indices grow per thread: last wins
+    } else if (abs_err > p.max_abs) {
+        p.max_abs = abs_err;
+        p.argmax = i;
+    }
+    if (rel_err != rel_err) p.nan_rel = (long long)i;
+    else if (rel_err > p.max_rel) p.max_rel = rel_err;
+}
+
+// Each block owns one contiguous chunk; threads stride within it, so a
+// thread's indices are increasing (needed for the nan_* "last" updates).
+extern "C" __global__ void __launch_bounds__(KTC_VERIFY_THREADS)
+ktc_verify_partial(const void* __restrict__ cand, const void* __restrict__ ref,
+                   unsigned long long n, int is_f32, double rel_tol, double abs_tol,
+                   VerifyPartial* __restrict__ partials) {
+    VerifyPartial p;
+    vp_init(p);
+    const unsigned long long chunk = (n + gridDim.x - 1) / gridDim.x;
+    const unsigned long long begin = chunk * blockIdx.x;
+    const unsigned long long end = begin + chunk < n ? begin + chunk : n;
+    if (is_f32) {
+        const float* c = (const float*)cand;
+        const float* r = (const float*)ref;
+        for (unsigned long long i = begin + threadIdx.x; i < end; i += KTC_VERIFY_THREADS)
+            vp_element<true>(p, i, (double)__ldg(c + i), (double)__ldg(r + i), rel_tol, abs_tol,
+                             false);
+    } else {
+        const int* c = (const int*)cand;
+        const int* r = (const int*)ref;
+        for (unsigned long long i = begin + threadIdx.x; i < end; i += KTC_VERIFY_THREADS) {
+            const int ci = __ldg(c + i), ri = __ldg(r + i);
+            vp_element<false>(p, i, (double)ci, (double)ri, 0.0, 0.0, ci == ri);
+        }
+    }
+    vp_block_reduce(p, partials + blockIdx.x);
+}
+
+extern "C" __global__ void __launch_bounds__(KTC_VERIFY_THREADS)
+ktc_verify_final(const VerifyPartial* __restrict__ partials, int count,
+                 VerifyPartial* __restrict__ result) {
+    VerifyPartial p;
+    vp_init(p);
+    for (int i = threadIdx.x; i < count; i += KTC_VERIFY_THREADS) vp_merge(p, partials[i]);
+    vp_block_reduce(p, result);
+}
+
+// Second pass, only run when a NaN error occurred before the last element:
+// the reference's running max restarts after the last NaN (tuner.hpp:53-62),
+// so the reported maximum is the max over the suffix (start, n).
+extern "C" __global__ void __launch_bounds__(KTC_VERIFY_THREADS)
+ktc_verify_after(const void* __restrict__ cand, const void* __restrict__ ref,
+                 unsigned long long n, int is_f32, long long abs_start, long long rel_start,
+                 VerifyPartial* __restrict__ partials) {
+    VerifyPartial p;
+    vp_init(p);
+    const unsigned long long stride = (unsigned long long)gridDim.x * KTC_VERIFY_THREADS;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * KTC_VERIFY_THREADS + threadIdx.x;
+         i < n; i += stride) {
+        double c, r;
+        if (is_f32) {
+            c = (double)((const float*)cand)[i];
+            r = (double)((const float*)ref)[i];
+        } else {
+            c = (double)((const int*)cand)[i];
+            r = (double)((const int*)ref)[i];
+        }
+        const double abs_err = fabs(c - r);
+        double rel_err = abs_err;
+        if (is_f32) {
+            const double mag = fabs(r);
+            rel_err = mag > 0.0 ? abs_err / mag : 0.0;
+        }
+        if ((long long)i > abs_start && abs_err > p.max_abs) p.max_abs = abs_err;
+        if ((long long)i > rel_start && rel_err > p.max_rel) p.max_rel = rel_err;
+    }
+    vp_block_reduce(p, partials + blockIdx.x);
+}
+
+// ---------------------------------------------------------------------------
+// L2 flush: read `n4` float4s; the never-taken store keeps the loads alive.
+// ---------------------------------------------------------------------------
+extern "C" __global__ void ktc_l2_flush(const float4* __restrict__ buf, unsigned long long n4,
+                                        float* __restrict__ sink) {
+    float s = 0.0f;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += stride) {
+        const float4 v = buf[i];  // normal caching: displaces resident lines
+        s += v.x + v.y + v.z + v.w;
+    }
+    if (s == -1.0f) *sink = s;  // buffer holds zeros: never true
+}

@@ -1,0 +1,216 @@
+// gemm.cu -- tunable fp32 SGEMM family, compiled at tuning time by NVRTC for
+// sm_100a, one specialization per configuration of gemm_space() (reference
+// landscapes.hpp:218-249).  Computes gemm_apply (landscapes.hpp:293-312):
+//     Cout[m*N + n] = ALPHA * sum_k A[k*M + m] * B[k*N + n] + BETA * Cin[m*N + n]
+// with A stored K x M (M contiguous), B K x N (N contiguous), C M x N (N
+// contiguous).  fp32 FFMA on the CUDA cores only, so the result is
+// comparable to the fp32 oracle within the reference's default tolerance.
+//
+// Parameters (compile-time -D defines, semantics of the paper's Sec. VI-A):
+//   MWG, NWG, KWG   C tile per thread block (M x N) and K step per iteration
+//   MDIMC, NDIMC    thread block; each thread owns an MWI x NWI register tile
+//                   (MWI = MWG/MDIMC, NWI = NWG/NDIMC)
+//   SA, SB          stage the A / B tile of each K step in shared memory
+//   MDIMA, NDIMB    thread re-shape used for those shared-memory copies:
+//                   MDIMA x KDIMA over the A tile, KDIMB x NDIMB over the B
+//                   tile (KDIMA = MDIMC*NDIMC/MDIMA, KDIMB = MDIMC*NDIMC/NDIMB)
+//   STRM, STRN      0: a thread's vectors along M (N) are contiguous;
+//                   1: they are MDIMC (NDIMC) vectors apart -- consecutive
+//                   threads then touch consecutive vectors
+//   VWM, VWN        vector width of A (M) and B/C (N) accesses
+//   KWI             unroll factor of the inner K loop
+// C is N-contiguous, so output stores vectorize along N (VWN).
+
+#define MWI (MWG / MDIMC)
+#define NWI (NWG / NDIMC)
+#define NT (MDIMC * NDIMC)
+#define MVI (MWI / VWM)  // A vectors per thread per k
+#define NVI (NWI / VWN)  // B vectors per thread per k
+
+#if SA
+#define KDIMA (NT / MDIMA)
+#define KWA (KWG / KDIMA)
+#define VA (MWG / VWM)                          // A vectors per k-row of the tile
+#define MVA ((VA >= MDIMA) ? (VA / MDIMA) : 1)  // per copying thread
+#endif
+#if SB
+#define KDIMB (NT / NDIMB)
+#define KWB (KWG / KDIMB)
+#define VB (NWG / VWN)
+#define NVB ((VB >= NDIMB) ? (VB / NDIMB) : 1)
+#endif
+
+template <int N>
+__device__ __forceinline__ void vload(float* d, const float* p) {
+    if (N == 1) {
+        d[0] = p[0];
+    } else if (N == 2) {
+        const float2 v = *reinterpret_cast<const float2*>(p);
+        d[0] = v.x; d[1] = v.y;
+    } else {
+#pragma unroll
+        for (int q = 0; q < N; q += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(p + q);
+            d[q] = v.x; d[q + 1] = v.y; d[q + 2] = v.z; d[q + 3] = v.w;
+        }
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void vload_g(float* d, const float* __restrict__ p) {
+    if (N == 1) {
+        d[0] = __ldg(p);
+    } else if (N == 2) {
+        const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+        d[0] = v.x; d[1] = v.y;
+    } else {
+#pragma unroll
+        for (int q = 0; q < N; q += 4) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(p + q));
+            d[q] = v.x; d[q + 1] = v.y; d[q + 2] = v.z; d[q + 3] = v.w;
+        }
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void vstore(float* p, const float* s) {
+    if (N == 1) {
+        p[0] = s[0];
+    } else if (N == 2) {
+        *reinterpret_cast<float2*>(p) = make_float2(s[0], s[1]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < N; q += 4)
+            *reinterpret_cast<float4*>(p + q) = make_float4(s[q], s[q + 1], s[q + 2], s[q + 3]);
+    }
+}
+
+extern "C" __global__ void __launch_bounds__(NT, 1)
+gemm(const int M, const int N, const int K, const float alpha, const float beta,
+     const float* __restrict__ A, const float* __restrict__ B, const float* __restrict__ Cin,
+     float* __restrict__ Cout) {
+    const int tx = threadIdx.x;  // along M
+    const int ty = threadIdx.y;  // along N
+    const int m0 = blockIdx.x * MWG;
+    const int n0 = blockIdx.y * NWG;
+
+#if SA || SB
+    extern __shared__ __align__(16) float smem[];
+    const int tid = ty * MDIMC + tx;
+#endif
+#if SA
+    float* alm = smem;  // [KWG][MWG]
+#endif
+#if SB
+    float* blm = smem + SA * KWG * MWG;  // [KWG][NWG]
+#endif
+
+    float acc[MWI][NWI];
+#pragma unroll
+    for (int i = 0; i < MWI; ++i)
+#pragma unroll
+        for (int j = 0; j < NWI; ++j) acc[i][j] = 0.0f;
+
+#pragma unroll 1
+    for (int k0 = 0; k0 < K; k0 += KWG) {
+#if SA
+        {
+            const int la0 = tid % MDIMA, la1 = tid / MDIMA;
+            if (VA >= MDIMA || la0 < VA) {
+#pragma unroll
+                for (int kia = 0; kia < KWA; ++kia) {
+                    const int k = la1 * KWA + kia;
+#pragma unroll
+                    for (int mia = 0; mia < MVA; ++mia) {
+                        const int mv = STRM ? (la0 + mia * MDIMA) : (mia + la0 * MVA);
+                        float v[VWM];
+                        vload_g<VWM>(v, A + (size_t)(k0 + k) * M + m0 + mv * VWM);
+                        vstore<VWM>(alm + k * MWG + mv * VWM, v);
+                    }
+                }
+            }
+        }
+#endif
+#if SB
+        {
+            const int lb0 = tid % NDIMB, lb1 = tid / NDIMB;
+            if (VB >= NDIMB || lb0 < VB) {
+#pragma unroll
+                for (int kib = 0; kib < KWB; ++kib) {
+                    const int k = lb1 * KWB + kib;
+#pragma unroll
+                    for (int nib = 0; nib < NVB; ++nib) {
+                        const int nv = STRN ? (lb0 + nib * NDIMB) : (nib + lb0 * NVB);
+                        float v[VWN];
+                        vload_g<VWN>(v, B + (size_t)(k0 + k) * N + n0 + nv * VWN);
+                        vstore<VWN>(blm + k * NWG + nv * VWN, v);
+                    }
+                }
+            }
+        }
+#endif
+#if SA || SB
+        __syncthreads();
+#endif
+
+#pragma unroll 1
+        for (int kw = 0; kw < KWG; kw += KWI) {
+#pragma unroll
+            for (int ki = 0; ki < KWI; ++ki) {
+                const int k = kw + ki;
+                float a[MWI], b[NWI];
+#pragma unroll
+                for (int mi = 0; mi < MVI; ++mi) {
+                    const int mv = STRM ? (tx + mi * MDIMC) : (mi + tx * MVI);
+#if SA
+                    vload<VWM>(a + mi * VWM, alm + k * MWG + mv * VWM);
+#else
+                    vload_g<VWM>(a + mi * VWM, A + (size_t)(k0 + k) * M + m0 + mv * VWM);
+#endif
+                }
+#pragma unroll
+                for (int ni = 0; ni < NVI; ++ni) {
+                    const int nv = STRN ? (ty + ni * NDIMC) : (ni + ty * NVI);
+#if SB
+                    vload<VWN>(b + ni * VWN, blm + k * NWG + nv * VWN);
+#else
+                    vload_g<VWN>(b + ni * VWN, B + (size_t)(k0 + k) * N + n0 + nv * VWN);
+#endif
+                }
+#pragma unroll
+                for (int i = 0; i < MWI; ++i)
+#pragma unroll
+                    for (int j = 0; j < NWI; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+            }
+        }
+#if SA || SB
+        __syncthreads();
+#endif
+    }
+
+    // Epilogue: Cout = alpha * acc + beta * Cin, VWN-wide stores along N.
+#pragma unroll
+    for (int mi = 0; mi < MVI; ++mi) {
+        const int mv = STRM ? (tx + mi * MDIMC) : (mi + tx * MVI);
+#pragma unroll
+        for (int e = 0; e < VWM; ++e) {
+            const int m = m0 + mv * VWM + e;
+#pragma unroll
+            for (int ni = 0; ni < NVI; ++ni) {
+                const int nv = STRN ? (ty + ni * NDIMC) : (ni + ty * NVI);
+                const size_t idx = (size_t)m * N + n0 + nv * VWN;
+                float s[VWN];
+                if (beta != 0.0f) {
+                    float c[VWN];
+                    vload_g<VWN>(c, Cin + idx);
+#pragma unroll
+                    for (int q = 0; q < VWN; ++q) s[q] = alpha * acc[mi * VWM + e][ni * VWN + q] + beta * c[q];
+                } else {
+#pragma unroll
+                    for (int q = 0; q < VWN; ++q) s[q] = alpha * acc[mi * VWM + e][ni * VWN + q];
+                }
+                vstore<VWN>(Cout + idx, s);
+            }
+        }
+    }
+}
