@@ -494,8 +494,11 @@ void ensure_backends(ktc_tuner* t) {
         o.abs_tol = t->job.abs_tol;
         for (int d : t->devices) t->backends.push_back(std::make_unique<CudaBackend>(d, &o));
     } else if (t->backend_spec.rfind("replay:", 0) == 0) {
-        t->backends.push_back(
-            std::make_unique<ReplayBackend>(ReplayBackend::load(t->backend_spec.substr(7))));
+        // One replay worker per listed "device": exercises the sharded
+        // executor on hosts without GPUs (tests of the merge rule).
+        const ReplayBackend proto = ReplayBackend::load(t->backend_spec.substr(7));
+        for (size_t i = 0; i < t->devices.size(); ++i)
+            t->backends.push_back(std::make_unique<ReplayBackend>(proto.table()));
     } else {
         throw BackendUnavailable(t->backend_spec);
     }

@@ -1,0 +1,214 @@
+"""Parity of the B200 path with the oracle (GPU).
+
+* the device reference kernels are BIT-EXACT with the reference's CPU
+  oracle (FNV digests vs the golden digests the reference produced);
+* every evaluated configuration of both kernel families matches the oracle
+  within the stated fp32 tolerance (rel 1e-4, abs 1e-6: the reference
+  defaults, tuner.hpp:148-149), checked on the device AND re-checked here on
+  the host against the C oracle;
+* the device verifier reproduces verify_outputs' report field for field.
+"""
+import random
+
+import numpy as np
+import pytest
+
+import paper_1703_06503_b200 as pkg
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def conv_configs(f, n, seed, device="B200"):
+    t = pkg.Tuner.conv(512, 256, f, device=device)
+    _, _, valid = t.space_counts()
+    rng = random.Random(seed)
+    return [pkg.parse_canonical(t.space_config(i)) for i in sorted(rng.sample(range(valid), n))]
+
+
+def gemm_configs(n, seed, m=256):
+    t = pkg.Tuner.gemm(m, m, m, device="B200")
+    _, _, valid = t.space_counts()
+    rng = random.Random(seed)
+    return [pkg.parse_canonical(t.space_config(i)) for i in sorted(rng.sample(range(valid), n))]
+
+
+# --------------------------------------------------------------- references
+@pytest.mark.parametrize("f", [3, 5, 7, 9, 11])
+def test_device_conv_reference_bit_exact(backend, golden, f):
+    cfg = dict(XWG=32, YWG=8, XWPT=1, YWPT=1, LOCAL=0, VW=1, PAD=0, UNR=1)
+    req = pkg.conv_request(8192, 4096, f, cfg)
+    _, dig = backend.read_reference(req, 8192 * 4096)
+    assert dig == golden["conv_digests"][str(f)]
+
+
+@pytest.mark.parametrize("m", [512, 1024, 2048])
+def test_device_gemm_reference_bit_exact(backend, golden, m):
+    cfg = dict(MWG=64, NWG=64, KWG=16, MDIMC=16, NDIMC=16, SA=1, SB=1, MDIMA=16, NDIMB=16,
+               STRM=0, STRN=0, VWM=1, VWN=1, KWI=2)
+    _, dig = backend.read_reference(pkg.gemm_request(m, m, m, cfg), m * m)
+    assert dig == golden["gemm_digests"][str(m)]
+
+
+def test_device_reference_small_cases(backend, golden):
+    for case in golden["small"]:
+        if case["kind"] == "conv":
+            x, y, f = case["x"], case["y"], case["f"]
+            cfg = dict(XWG=8, YWG=8, XWPT=1, YWPT=1, LOCAL=0, VW=1, PAD=0, UNR=0)
+            req = pkg.conv_request(x, y, f, cfg, w=case["w"], seed=case["seed"])
+            _, dig = backend.read_reference(req, x * y)
+        else:
+            m, n, k = case["m"], case["n"], case["k"]
+            cfg = dict(MWG=16, NWG=16, KWG=16, MDIMC=8, NDIMC=8, SA=0, SB=0, MDIMA=8, NDIMB=8,
+                       STRM=0, STRN=0, VWM=1, VWN=1, KWI=2)
+            req = pkg.gemm_request(m, n, k, cfg, alpha=case["alpha"], beta=case["beta"],
+                                   seed=case["seed"])
+            _, dig = backend.read_reference(req, m * n)
+        assert dig == case["digest"], case
+
+
+# ------------------------------------------------------------- conv family
+@pytest.mark.parametrize("f", [3, 7, 11])
+def test_conv_configs_match_oracle(backend, f):
+    x, y = 512, 256
+    want = O.conv_reference(x, y, f)
+    bad = []
+    for cfg in conv_configs(f, 40, seed=f):
+        r = backend.evaluate(pkg.conv_request(x, y, f, cfg))
+        if not (r.ok and r.verification == "pass"):
+            bad.append((cfg, r.status, r.verification, r.message))
+            continue
+        rep = O.verify(backend.read_output(x * y), want)
+        if not rep["pass"]:
+            bad.append((cfg, "host", rep))
+    assert not bad, bad[:5]
+
+
+def test_conv_paper_rows_and_edge_tiles(backend):
+    """Table II rows plus the extreme tile shapes, incl. ragged images (GUARD)."""
+    rows = [
+        dict(XWG=32, YWG=8, XWPT=1, YWPT=8, LOCAL=0, VW=1, PAD=0, UNR=1),
+        dict(XWG=32, YWG=16, XWPT=2, YWPT=4, LOCAL=2, VW=2, PAD=1, UNR=1),
+        dict(XWG=32, YWG=8, XWPT=2, YWPT=8, LOCAL=2, VW=2, PAD=1, UNR=1),
+        dict(XWG=64, YWG=8, XWPT=1, YWPT=4, LOCAL=0, VW=1, PAD=0, UNR=1),
+        dict(XWG=32, YWG=8, XWPT=2, YWPT=4, LOCAL=1, VW=2, PAD=0, UNR=1),
+        dict(XWG=64, YWG=8, XWPT=8, YWPT=8, LOCAL=2, VW=8, PAD=1, UNR=1),    # 512-wide, 4 panels
+        dict(XWG=8, YWG=64, XWPT=8, YWPT=8, LOCAL=2, VW=4, PAD=0, UNR=1),    # 512-tall, 3 boxes
+        dict(XWG=64, YWG=8, XWPT=8, YWPT=8, LOCAL=1, VW=8, PAD=1, UNR=0),
+        dict(XWG=8, YWG=8, XWPT=1, YWPT=1, LOCAL=1, VW=1, PAD=1, UNR=0),
+    ]
+    for (x, y, f) in [(512, 512, 3), (1024, 512, 11), (520, 300, 7)]:
+        want = O.conv_reference(x, y, f)
+        for cfg in rows:
+            gx = -(-x // cfg["XWPT"])
+            gy = -(-y // cfg["YWPT"])
+            req = pkg.conv_request(x, y, f, cfg)
+            req.global_size = (gx, gy)
+            r = backend.evaluate(req)
+            assert r.ok and r.verification == "pass", (x, y, f, cfg, r)
+            assert O.verify(backend.read_output(x * y), want)["pass"], (x, y, f, cfg)
+
+
+def test_conv_full_size_best_known(backend):
+    for f, cfg in [(3, dict(XWG=32, YWG=8, XWPT=1, YWPT=8, LOCAL=0, VW=1, PAD=0, UNR=1)),
+                   (11, dict(XWG=32, YWG=8, XWPT=2, YWPT=8, LOCAL=2, VW=2, PAD=1, UNR=1))]:
+        r = backend.evaluate(pkg.conv_request(8192, 4096, f, cfg, reps=3))
+        assert r.ok and r.verification == "pass", r
+        assert r.report["elements_compared"] == 8192 * 4096
+        assert r.report["max_rel_error"] < 1e-4
+
+
+# ------------------------------------------------------------- gemm family
+def test_gemm_configs_match_oracle(backend):
+    m = 256
+    want = O.gemm_reference(m, m, m)
+    bad = []
+    for cfg in gemm_configs(60, seed=1, m=m):
+        r = backend.evaluate(pkg.gemm_request(m, m, m, cfg))
+        if not (r.ok and r.verification == "pass"):
+            bad.append((cfg, r.status, r.verification, r.message))
+            continue
+        if not O.verify(backend.read_output(m * m), want)["pass"]:
+            bad.append((cfg, "host"))
+    assert not bad, bad[:5]
+
+
+def test_gemm_paper_rows_beta_and_rectangular(backend):
+    rows = [(128, 128, 16, 16, 16, 1, 1, 32, 16, 1, 0, 2, 1, 8),
+            (64, 64, 32, 8, 16, 1, 1, 32, 32, 1, 0, 2, 2, 8),
+            (128, 128, 32, 16, 16, 1, 1, 32, 32, 0, 1, 4, 4, 2),
+            (64, 64, 16, 8, 8, 1, 1, 8, 16, 1, 1, 4, 4, 8),
+            (128, 128, 128, 8, 8, 1, 1, 8, 8, 1, 1, 8, 8, 8),
+            (16, 16, 16, 32, 32, 0, 1, 8, 32, 0, 1, 1, 1, 2)]
+    names = "MWG NWG KWG MDIMC NDIMC SA SB MDIMA NDIMB STRM STRN VWM VWN KWI".split()
+    for (m, n, k, a, b) in [(256, 384, 128, 1.0, 0.0), (512, 128, 256, 1.5, 0.5)]:
+        want = O.gemm_reference(m, n, k, a, b)
+        for row in rows:
+            cfg = dict(zip(names, row))
+            r = backend.evaluate(pkg.gemm_request(m, n, k, cfg, alpha=a, beta=b))
+            assert r.ok and r.verification == "pass", (cfg, r)
+            assert O.verify(backend.read_output(m * n), want)["pass"], cfg
+
+
+def test_gemm_indivisible_problem_is_runtime_error(backend):
+    cfg = dict(MWG=128, NWG=128, KWG=16, MDIMC=16, NDIMC=16, SA=1, SB=1, MDIMA=16, NDIMB=16,
+               STRM=1, STRN=1, VWM=4, VWN=4, KWI=8)
+    req = pkg.gemm_request(256, 256, 256, cfg)
+    req.args = pkg.backend.gemm_args(200, 256, 256)
+    req.global_size = (200 * 16 // 128, 256 * 16 // 128)
+    r = backend.evaluate(req)
+    assert r.status == "runtime_error" and "multiple" in r.message
+
+
+# --------------------------------------------------- device verifier parity
+def _cases():
+    rng = np.random.default_rng(5)
+    ref = rng.random(100_003, dtype=np.float32) * 4 - 2
+    c0 = ref.copy()
+    c1 = ref * (1 + 5e-5)                          # passes
+    c2 = ref.copy(); c2[777] += 1.0                # fails at 777
+    c3 = ref.copy(); c3[5] = np.nan                # NaN mid-buffer
+    c4 = ref.copy(); c4[-1] = np.nan               # NaN last -> max is NaN
+    c5 = ref.copy(); c5[10] = np.nan; c5[99_000] = np.nan; c5[99_001] += 3.0
+    z = np.zeros(1000, np.float32)
+    z1 = z.copy(); z1[3] = 5e-7                    # abs tolerance near zero: pass
+    z2 = z.copy(); z2[3] = 2e-6                    # fail
+    inf = ref.copy(); inf[42] = np.inf
+    ties = ref.copy(); ties[100] += 1e-5; ties[200] += 1e-5   # argmax tie -> first index
+    return [(c0, ref), (c1, ref), (c2, ref), (c3, ref), (c4, ref), (c5, ref), (z1, z), (z2, z),
+            (inf, ref), (ties.astype(np.float32), ref), (np.zeros(0, np.float32), np.zeros(0, np.float32))]
+
+
+def test_device_verifier_matches_host_rule(backend):
+    for cand, ref in _cases():
+        cand = np.ascontiguousarray(cand, np.float32)
+        want = O.verify(cand, ref)
+        got = backend.verify_pair(cand, ref)
+        for key in ("pass", "buffer_index", "element_index", "elements_compared"):
+            assert got[key] == want[key], (key, got, want)
+        for key in ("max_abs_error", "max_rel_error"):
+            a, b = got[key], want[key]
+            assert (np.isnan(a) and np.isnan(b)) or a == b, (key, got, want)
+
+
+def test_device_verifier_i32(backend):
+    ref = np.arange(5000, dtype=np.int32)
+    cand = ref.copy(); cand[1234] += 2
+    got = backend.verify_pair(cand, ref)
+    want = O.verify(cand, ref)
+    assert got == want
+
+
+# ----------------------------------------------------- tuner end-to-end
+def test_tuner_random_search_conv_verified(built):
+    t = pkg.Tuner.conv(1024, 512, 5, devices=[0])
+    t.UseRandomSearch(1 / 128)
+    t.SetVerification(True)
+    s = t.Tune()
+    rows = t.rows()
+    assert s["rows"] == len(rows) == s["budget"] == 5104 // 128
+    assert all(r.status == "ok" and r.verified == "pass" for r in rows), \
+        [(r.config, r.status, r.message) for r in rows if r.status != "ok" or r.verified != "pass"]
+    best, ms = t.GetBestResult()
+    assert ms == min(r.time_ms for r in rows)
+    assert s["kernel_launches"] > 0

@@ -1,0 +1,166 @@
+"""Search layer parity with the reference tuner (CPU).
+
+Both tuners run the SAME job (the reference's JSON format) on the SAME
+per-configuration times: a replay table priced by the reference's own
+synthetic cost model (with injected failures, which replay as `missing`).
+The results CSVs must be byte-identical: same enumeration order, same RNG
+consumption in random / annealing / PSO, same cache and tie rules, same
+running bests and report format.  The sharded executor (several workers,
+dynamic chunks) must reproduce the sequential CSV exactly.
+"""
+import json
+from pathlib import Path
+
+import pytest
+
+import paper_1703_06503_b200 as pkg
+from oracle import oracle as O
+
+pytestmark = pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+
+B200 = {"name": "B200", "max_work_group_total": 1024, "max_work_group_dim": [1024, 1024, 64],
+        "local_mem_bytes": 232448}
+
+
+def price(tmp: Path, job: dict, model: str, failure_rate=0.0, name="table.csv") -> str:
+    j = dict(job)
+    j["backend"] = {"kind": "synthetic", "model": model, "failure_rate": failure_rate}
+    O.ref_job_price_table(json.dumps(j), str(tmp / name))
+    return name
+
+
+def run_both(tmp: Path, job: dict, devices=(0,)):
+    text = json.dumps(job)
+    ref_csv = tmp / "ref.csv"
+    bi, bt = O.ref_job_run(text, str(tmp), str(ref_csv))
+    t = pkg.Tuner.from_job(text, str(tmp), devices=list(devices))
+    t.Tune()
+    mine_csv = tmp / "mine.csv"
+    t.write_csv(str(mine_csv))
+    return ref_csv.read_bytes(), mine_csv.read_bytes(), (bi, bt), t
+
+
+CONV = {"template": "conv", "problem": {"filter": 5}, "device": B200}
+
+
+@pytest.fixture(scope="module")
+def conv_table(tmp_path_factory):
+    d = tmp_path_factory.mktemp("conv")
+    price(d, CONV, "conv-like", failure_rate=0.07)
+    return d
+
+
+@pytest.mark.parametrize("strategy", [
+    {"kind": "full"},
+    {"kind": "random", "fraction": "1/32"},
+    {"kind": "random", "fraction": 0.25},
+    {"kind": "annealing", "fraction": "1/64", "temperature": 4},
+    {"kind": "annealing", "fraction": "1/16", "temperature": 0.5},
+    {"kind": "pso", "fraction": "1/64"},
+    {"kind": "pso", "fraction": "1/32", "swarm": 5, "alpha": 0.3, "beta": 0.3, "gamma": 0.3},
+])
+@pytest.mark.parametrize("seed", [1, 7])
+def test_conv_strategies_byte_identical(conv_table, strategy, seed):
+    job = dict(CONV, backend={"kind": "replay", "path": "table.csv"}, strategy=strategy, seed=seed)
+    ref, mine, (bi, bt), t = run_both(conv_table, job)
+    assert mine == ref
+    s = t.summary()
+    assert s["best_index"] == bi and s["best_time_ms"] == bt
+
+
+@pytest.mark.parametrize("strategy", [{"kind": "full"}, {"kind": "random", "fraction": "1/8"}])
+@pytest.mark.parametrize("devices", [(0, 1), (0, 1, 2, 3), tuple(range(8))])
+def test_sharded_executor_reproduces_sequential(conv_table, strategy, devices):
+    job = dict(CONV, backend={"kind": "replay", "path": "table.csv"}, strategy=strategy, seed=3)
+    ref, mine, (bi, _), t = run_both(conv_table, job, devices=devices)
+    assert mine == ref
+    assert t.summary()["best_index"] == bi
+
+
+def test_golden_conv_winner_full_search(tmp_path, golden):
+    # conv f=3, B200 limits, reference synthetic conv-like model.
+    job = {"template": "conv", "problem": {"filter": 3}, "device": B200}
+    price(tmp_path, job, "conv-like")
+    job.update(backend={"kind": "replay", "path": "table.csv"}, strategy={"kind": "full"})
+    t = pkg.Tuner.from_job(json.dumps(job), str(tmp_path), devices=[0, 1, 2, 3])
+    s = t.Tune()
+    w = golden["winners"]["conv_f3_B200_conv_like"]
+    assert s["rows"] == w["rows"]
+    assert s["best_index"] + 1 == w["best_step"]
+    assert t.GetBestResult()[0] == w["best_config"]
+
+
+@pytest.mark.slow
+def test_golden_gemm_winner_full_search_852k(tmp_path, golden):
+    # 852,608-row full search of the GEMM space at 4096^3, sharded 8 ways.
+    job = {"template": "gemm", "problem": {"m": 4096, "n": 4096, "k": 4096}, "device": B200}
+    price(tmp_path, job, "gemm-like")
+    job.update(backend={"kind": "replay", "path": "table.csv"}, strategy={"kind": "full"})
+    t = pkg.Tuner.from_job(json.dumps(job), str(tmp_path), devices=list(range(8)))
+    s = t.Tune()
+    w = golden["winners"]["gemm_4096_B200_gemm_like"]
+    assert s["rows"] == w["rows"] == 852608
+    assert s["best_index"] + 1 == w["best_step"]
+    cfg, ms = t.GetBestResult()
+    assert cfg == w["best_config"] and ms == w["best_time_ms"]
+
+
+def test_gemm_random_and_annealing_byte_identical(tmp_path):
+    job = {"template": "gemm", "problem": {"m": 1024, "n": 1024, "k": 1024}, "device": "K40m",
+           "space": {"constraints": ["MWG >= 64", "NWG >= 64", "KWI == 8"]}}
+    price(tmp_path, job, "gemm-like", failure_rate=0.05)
+    for strategy in ({"kind": "random", "fraction": "1/256"},
+                     {"kind": "annealing", "fraction": "1/2048", "temperature": 4},
+                     {"kind": "pso", "fraction": "1/2048"}):
+        j = dict(job, backend={"kind": "replay", "path": "table.csv"}, strategy=strategy, seed=2)
+        ref, mine, _, _ = run_both(tmp_path, j)
+        assert mine == ref, strategy
+
+
+def test_custom_kernel_space_byte_identical(tmp_path):
+    job = {
+        "kernel": {"name": "copy", "source_ref": "copy.cu", "global": [4096, 64], "local": [1, 1],
+                   "modifiers": [{"target": "global", "op": "divide", "factors": ["WPT", "1"]},
+                                 {"target": "local", "op": "multiply", "factors": ["TBX", "TBY"]}],
+                   "local_mem": "4 * TBX * TBY * (PAD + 1)",
+                   "arguments": [{"role": "input", "type": "f32", "length": 4096, "fill": "ramp"},
+                                 {"role": "output", "type": "f32", "length": 4096}]},
+        "space": {"parameters": {"WPT": [1, 2, 3, 4, 8], "TBX": [8, 16, 32, 64, 128],
+                                 "TBY": [1, 2, 4, 8], "PAD": [0, 1, 2]},
+                  "constraints": ["TBX * TBY <= 256 || PAD == 0", "!(WPT == 8 && TBY > 2)",
+                                  "(WPT + TBX) % 3 != 1 || TBY == 1"]},
+        "device": {"name": "tiny", "max_work_group_total": 512,
+                   "max_work_group_dim": [256, 4, 1], "local_mem_bytes": 4096},
+    }
+    price(tmp_path, job, "hash-random", failure_rate=0.1)
+    for strategy in ({"kind": "full"}, {"kind": "random", "fraction": "1/3"},
+                     {"kind": "annealing", "fraction": "1/4"}, {"kind": "pso", "fraction": "1/4"}):
+        j = dict(job, backend={"kind": "replay", "path": "table.csv"}, strategy=strategy)
+        ref, mine, _, _ = run_both(tmp_path, j)
+        assert mine == ref, strategy
+
+
+def test_enumeration_order_matches_reference(tmp_path):
+    job = {"template": "conv", "problem": {"filter": 9}, "device": "K40m"}
+    want = O.ref_job_enumerate(json.dumps(job), tmp_path / "e.txt")
+    t = pkg.Tuner.from_job(json.dumps(job), str(tmp_path))
+    assert [t.space_config(i) for i in range(len(want))] == want
+    job = {"template": "gemm", "device": "HD7970"}
+    want = O.ref_job_enumerate(json.dumps(job), tmp_path / "g.txt")
+    t = pkg.Tuner.from_job(json.dumps(job), str(tmp_path))
+    assert len(want) == t.space_counts()[2] == 639368
+    for i in list(range(0, len(want), 9973)) + [len(want) - 1]:
+        assert t.space_config(i) == want[i]
+
+
+def test_space_counts_golden(golden):
+    jobs = {
+        "conv_f3_B200": {"template": "conv", "problem": {"filter": 3}, "device": B200},
+        "conv_f11_K40m": {"template": "conv", "problem": {"filter": 11}, "device": "K40m"},
+        "gemm_4096_B200": {"template": "gemm", "problem": {"m": 4096, "n": 4096, "k": 4096},
+                           "device": B200},
+        "gemm_2048_HD7970": {"template": "gemm", "device": "HD7970"},
+    }
+    for name, job in jobs.items():
+        t = pkg.Tuner.from_job(json.dumps(job), ".")
+        assert list(t.space_counts()) == golden["counts"][name], name
