@@ -15,6 +15,9 @@
 namespace ktb {
 
 using Evaluator = std::function<std::optional<double>(const Configuration&)>;
+// Optional hint: `config` is likely to be evaluated soon (compile it ahead).
+// Never changes what a strategy does -- only how early a backend starts work.
+using Prefetcher = std::function<void(const Configuration&)>;
 
 enum class StrategyKind { full, random, annealing, pso };
 const char* to_string(StrategyKind k);
@@ -56,11 +59,14 @@ SearchOutcome run_full(const SearchSpace& space, const Evaluator& evaluate);
 SearchOutcome run_random(const SearchSpace& space, const Evaluator& evaluate, double fraction,
                          uint64_t seed);
 SearchOutcome run_annealing(const SearchSpace& space, const Evaluator& evaluate,
-                            double temperature, double fraction, uint64_t seed);
+                            double temperature, double fraction, uint64_t seed,
+                            const Prefetcher& prefetch = nullptr);
 SearchOutcome run_pso(const SearchSpace& space, const Evaluator& evaluate, size_t swarm,
-                      double alpha, double beta, double gamma, double fraction, uint64_t seed);
+                      double alpha, double beta, double gamma, double fraction, uint64_t seed,
+                      const Prefetcher& prefetch = nullptr);
 SearchOutcome run_search(const SearchSpace& space, const Evaluator& evaluate,
-                         const StrategySpec& strategy, uint64_t seed);
+                         const StrategySpec& strategy, uint64_t seed,
+                         const Prefetcher& prefetch = nullptr);
 
 // The unit list a sharded executor distributes: the enumeration indices a
 // full search visits (0..N-1) or the random search's sample, in visit order.

@@ -73,6 +73,8 @@ class SearchSpace {
 
     Configuration random_valid(Rng& rng) const;
     Configuration random_neighbor(const Configuration& c, Rng& rng) const;
+    // The valid one-step neighbours random_neighbor draws from (no RNG use).
+    std::vector<Configuration> neighbors(const Configuration& c) const;
     std::vector<Configuration> sample_unique(size_t n, Rng& rng) const;
     // Enumeration indices of sample_unique's draw (same RNG consumption);
     // only for spaces within the enumeration limit.

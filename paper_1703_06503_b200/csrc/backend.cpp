@@ -68,19 +68,40 @@ struct Inputs {
 };
 
 struct Plan {
-    const std::string* src = nullptr;
-    std::string src_id;
-    std::vector<std::string> opts;
-    std::string entry;
+    const KernelSource* ksrc = nullptr;
+    Defines problem;  // shared by every configuration of a compile batch
+    Defines config;
     unsigned grid[3] = {1, 1, 1}, block[3] = {1, 1, 1};
     unsigned smem = 0;
-    int tma_mode = 0;  // 1: conv halo tile box (BW x BH)
+    int tma_mode = 0;  // 1: conv halo tile box (BW x BH); 2: tf32 A/B operand boxes
+    double rel_tol = -1.0;  // family tolerance override (< 0: backend options)
     unsigned box[2] = {0, 0};
 };
 
 std::string define(const char* name, long long v) {
-    return std::string("-D") + name + "=" + std::to_string(v);
+    return std::string(name) + "=" + std::to_string(v);
 }
+
+const KernelSource& conv_source() {
+    static const KernelSource s = split_source("conv.cu", kConvSource, "conv2d");
+    return s;
+}
+const KernelSource& gemm_source() {
+    static const KernelSource s = split_source("gemm.cu", kGemmSource, "gemm");
+    return s;
+}
+const KernelSource& tf32_source() {
+    static const KernelSource s = split_source("gemm_tf32.cu", kGemmTf32Source, "gemm_tf32");
+    return s;
+}
+
+// Loaded modules, most recently used last (a batch cubin serves several
+// configurations; c_taps is set once per module and argument list).
+struct ModuleEntry {
+    CubinPtr cubin;
+    CUmodule mod = nullptr;
+    std::string taps_sig;
+};
 
 }  // namespace
 
@@ -90,7 +111,8 @@ struct ktc_backend {
     std::string name;
     std::string cache_dir;
     std::unique_ptr<Inputs> in;
-    std::map<std::string, std::string> custom_sources;  // path -> text
+    std::map<std::string, KernelSource> custom_sources;  // path -> source
+    std::vector<ModuleEntry> modules;
 };
 
 namespace {
@@ -313,6 +335,7 @@ int build_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
 int ensure_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
     if (be->ctx->sticky) {
         free_inputs(be);
+        be->modules.clear();  // died with the context
         int st = ktc_reset(be->ctx);
         if (st) return st;
     }
@@ -362,11 +385,10 @@ bool plan_conv(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
         return false;
     }
     const long long H = (I.F - 1) / 2, TX = XWG * XWPT, TY = YWG * YWPT;
-    p->src = &kConvSource;
-    p->src_id = "conv.cu#" + std::to_string(std::hash<std::string>()(kConvSource));
-    p->entry = "conv2d";
-    auto& o = p->opts;
-    o = {define("FS", I.F), define("XWG", XWG), define("YWG", YWG), define("XWPT", XWPT),
+    p->ksrc = &conv_source();
+    p->problem = {define("FS", I.F)};
+    auto& o = p->config;
+    o = {define("XWG", XWG), define("YWG", YWG), define("XWPT", XWPT),
          define("YWPT", YWPT), define("LOCAL", LOCAL), define("VW", VW),
          define("PAD", LOCAL >= 1 ? PAD : 0), define("UNR", UNR ? 1 : 0),
          define("GUARD", (I.X % TX != 0 || I.Y % TY != 0) ? 1 : 0),
@@ -450,10 +472,8 @@ bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
     // cubin (they are still timed as separate rows).
     if (!SA) MDIMA = 8;
     if (!SB) NDIMB = 8;
-    p->src = &kGemmSource;
-    p->src_id = "gemm.cu#" + std::to_string(std::hash<std::string>()(kGemmSource));
-    p->entry = "gemm";
-    p->opts = {define("MWG", MWG),     define("NWG", NWG),     define("KWG", KWG),
+    p->ksrc = &gemm_source();
+    p->config = {define("MWG", MWG),     define("NWG", NWG),     define("KWG", KWG),
                define("MDIMC", MDIMC), define("NDIMC", NDIMC), define("SA", SA ? 1 : 0),
                define("SB", SB ? 1 : 0), define("MDIMA", MDIMA), define("NDIMB", NDIMB),
                define("STRM", v[9] ? 1 : 0), define("STRN", v[10] ? 1 : 0), define("VWM", VWM),
@@ -479,11 +499,11 @@ bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
     return true;
 }
 
-bool plan_gemm_tf32(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why);
 
 bool plan_custom(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why) {
     const std::string path = r->source_ref ? r->source_ref : "";
-    auto it = be->custom_sources.find(path);
+    const std::string entry = r->kernel_name ? r->kernel_name : "";
+    auto it = be->custom_sources.find(path + "|" + entry);
     if (it == be->custom_sources.end()) {
         std::ifstream f(path, std::ios::binary);
         if (!f) {
@@ -492,13 +512,16 @@ bool plan_custom(ktc_backend* be, const ktc_request* r, Plan* p, std::string* wh
         }
         std::ostringstream s;
         s << f.rdbuf();
-        it = be->custom_sources.emplace(path, s.str()).first;
+        KernelSource ks = split_source(path, s.str(), entry);
+        ks.prelude.clear();
+        ks.body = s.str();
+        ks.batchable = false;
+        ks.fixed_entry = entry;
+        it = be->custom_sources.emplace(path + "|" + entry, ks).first;
     }
-    p->src = &it->second;
-    p->src_id = path + "#" + std::to_string(std::hash<std::string>()(it->second));
-    p->entry = r->kernel_name;
+    p->ksrc = &it->second;
     for (int i = 0; i < r->n_params; ++i)
-        p->opts.push_back(define(r->param_names[i], r->param_values[i]));
+        p->config.push_back(define(r->param_names[i], r->param_values[i]));
     if (r->ndim < 1 || r->ndim > 3) {
         *why = "thread sizes must have 1 to 3 dimensions";
         return false;
@@ -514,21 +537,42 @@ bool plan_custom(ktc_backend* be, const ktc_request* r, Plan* p, std::string* wh
     return true;
 }
 
-}  // namespace
 
-// gemm_tf32.cpp provides the tcgen05 family plan and its launch.
-namespace ktc {
-bool plan_tf32(ktc_ctx* ctx, int M, int N, int K, const ktc_request* r, std::string* src_id,
-               const std::string** src, std::vector<std::string>* opts, std::string* entry,
-               unsigned grid[3], unsigned block[3], unsigned* smem, std::string* why);
-}
 
-namespace {
-
+// TF32 tcgen05 variant (kernels/gemm_tf32.cu): one 128-thread CTA per
+// 128 x BN tile, TMA tensor maps for A (M-major) and B (N-major), SWIZZLE_128B.
 bool plan_gemm_tf32(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why) {
     const Inputs& I = *be->in;
-    return ktc::plan_tf32(be->ctx, I.M, I.N, I.K, r, &p->src_id, &p->src, &p->opts, &p->entry,
-                          p->grid, p->block, &p->smem, why);
+    ParamView pv{r};
+    long long BN, BK, STAGES;
+    if (!pv.get("BN", &BN) || !pv.get("BK", &BK) || !pv.get("STAGES", &STAGES)) {
+        *why = "the gemm_tf32 family needs BN, BK, STAGES";
+        return false;
+    }
+    if (!(BN == 64 || BN == 128 || BN == 256) || !(BK == 32 || BK == 64) || STAGES < 2 ||
+        STAGES > 8) {
+        *why = "gemm_tf32 configuration outside the family's parameter domain";
+        return false;
+    }
+    if (I.M % 128 || I.N % BN || I.K % BK) {
+        *why = "problem size (" + std::to_string(I.M) + "x" + std::to_string(I.N) + "x" +
+               std::to_string(I.K) + ") is not a multiple of the (128, BN, BK) tile";
+        return false;
+    }
+    p->ksrc = &tf32_source();
+    p->config = {define("BN", BN), define("BK", BK), define("STAGES", STAGES)};
+    p->smem = unsigned(STAGES * 4 * BK * (128 + BN) + 2048);
+    if (p->smem > be->ctx->limits.smem_per_block_optin) {
+        *why = "needs " + std::to_string(p->smem) + " bytes of shared memory";
+        return false;
+    }
+    p->block[0] = 128;
+    p->grid[0] = unsigned(I.M / 128);
+    p->grid[1] = unsigned(I.N / BN);
+    p->tma_mode = 2;
+    p->box[0] = 32;
+    p->box[1] = unsigned(BK);
+    return true;
 }
 
 int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
@@ -562,30 +606,57 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
     // 1. cubin
     auto t0 = Clock::now();
     bool hit = false;
-    CubinPtr cubin = CompileService::instance().get(plan.src_id, *plan.src, plan.opts, &hit);
+    KernelPtr kern = CompileService::instance().get(*plan.ksrc, plan.problem, plan.config, &hit);
     out->compile_ms = hit ? 0.0 : ms_since(t0);
     out->compile_cache_hit = hit ? 1 : 0;
-    if (!cubin->ok()) {
+    if (!kern->ok()) {
         out->status = KTC_STATUS_COMPILE_ERROR;
-        set_msg(out, "NVRTC: " + cubin->log.substr(0, 480));
+        set_msg(out, "NVRTC: " + kern->log.substr(0, 480));
         return KTC_OK;
     }
 
-    // 2. module
+    // 2. module (cached per cubin: a compile batch serves several configs)
     t0 = Clock::now();
-    ktc_fn* fn = nullptr;
-    st = ktc_load(ctx, cubin->image.data(), cubin->image.size(), plan.entry.c_str(), &fn);
-    if (st) {
-        set_msg(out, last_error());
-        return ctx->sticky ? st : KTC_OK;
+    ModuleEntry* me = nullptr;
+    for (size_t i = 0; i < be->modules.size(); ++i)
+        if (be->modules[i].cubin.get() == kern->cubin.get()) {
+            std::rotate(be->modules.begin() + long(i), be->modules.begin() + long(i) + 1,
+                        be->modules.end());
+            me = &be->modules.back();
+            break;
+        }
+    if (!me) {
+        if (be->modules.size() >= 24) {
+            driver().cuModuleUnload(be->modules.front().mod);
+            be->modules.erase(be->modules.begin());
+        }
+        ModuleEntry e;
+        e.cubin = kern->cubin;
+        CUresult rc = driver().cuModuleLoadData(&e.mod, kern->cubin->image.data());
+        if (rc != CUDA_SUCCESS) {
+            st = fail_cu(ctx, rc, "cuModuleLoadData");
+            set_msg(out, last_error());
+            return ctx->sticky ? st : KTC_OK;
+        }
+        be->modules.push_back(e);
+        me = &be->modules.back();
     }
-    struct Unload {
-        ktc_fn* f;
-        ~Unload() { ktc_unload(f); }
-    } unload{fn};
+    ktc_fn fn_storage;
+    fn_storage.ctx = ctx;
+    fn_storage.mod = me->mod;
+    {
+        CUresult rc = driver().cuModuleGetFunction(&fn_storage.fn, me->mod, kern->entry.c_str());
+        if (rc != CUDA_SUCCESS) {
+            st = fail_cu(ctx, rc, "cuModuleGetFunction");
+            set_msg(out, last_error());
+            return ctx->sticky ? st : KTC_OK;
+        }
+    }
+    ktc_fn* fn = &fn_storage;
 
-    alignas(64) CUtensorMap tmap;
+    alignas(64) CUtensorMap tmap, tmap2;
     std::memset(&tmap, 0, sizeof(tmap));
+    std::memset(&tmap2, 0, sizeof(tmap2));
     std::vector<void*> params;
     // Scalar storage must outlive the launches.
     int iX = 0, iY = 0, iP = 0, iM = 0, iN = 0, iK = 0;
@@ -595,9 +666,12 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
     std::vector<float> scal_f;
     std::vector<CUdeviceptr> ptrs;
     if (fam == FAM_CONV) {
-        if (ktc_set_symbol(fn, "c_taps", I.taps.data(), I.taps.size() * 4) != KTC_OK) {
-            set_msg(out, last_error());
-            return ctx->sticky ? KTC_ERR_LAUNCH : KTC_OK;
+        if (me->taps_sig != I.sig) {
+            if (ktc_set_symbol(fn, "c_taps", I.taps.data(), I.taps.size() * 4) != KTC_OK) {
+                set_msg(out, last_error());
+                return ctx->sticky ? KTC_ERR_LAUNCH : KTC_OK;
+            }
+            me->taps_sig = I.sig;
         }
         if (plan.tma_mode == 1) {
             cuuint64_t dims[2] = {cuuint64_t(I.ipitch), cuuint64_t(I.rows)};
@@ -621,6 +695,24 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
         pOut = I.out[0];
         params = {&iX, &iY, &fW, &pImg, &iP, &pOut, &tmap};
     } else if (fam == FAM_GEMM || fam == FAM_GEMM_TF32) {
+        if (plan.tma_mode == 2) {
+            auto encode = [&](CUtensorMap* m, CUdeviceptr base, int inner, int outer) {
+                cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
+                cuuint64_t strides[1] = {cuuint64_t(inner) * 4};
+                cuuint32_t box[2] = {plan.box[0], plan.box[1]};
+                cuuint32_t estr[2] = {1, 1};
+                return d.cuTensorMapEncodeTiled(
+                    m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, reinterpret_cast<void*>(base), dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            };
+            CUresult rc = encode(&tmap, I.dev[5], I.M, I.K);
+            if (rc == CUDA_SUCCESS) rc = encode(&tmap2, I.dev[6], I.N, I.K);
+            if (rc != CUDA_SUCCESS) {
+                set_msg(out, cu_error_text(rc, "cuTensorMapEncodeTiled"));
+                return KTC_OK;
+            }
+        }
         iM = I.M;
         iN = I.N;
         iK = I.K;
@@ -631,6 +723,10 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
         pC = I.dev[7];
         pOut = I.out[0];
         params = {&iM, &iN, &iK, &fA, &fB, &pA, &pB, &pC, &pOut};
+        if (plan.tma_mode == 2) {
+            params.push_back(&tmap);
+            params.push_back(&tmap2);
+        }
     } else {
         st = refresh_custom_buffers(be);
         if (st) return st;
@@ -686,8 +782,7 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
         // Sticky faults poison the context: reset now so the next
         // configuration starts clean (inputs are rebuilt lazily).
         if (ctx->sticky) {
-            unload.f = nullptr;
-            delete fn;  // module died with the context
+            be->modules.clear();  // modules died with the context
             free_inputs(be);
             int rs = ktc_reset(ctx);
             if (rs) return rs;
@@ -710,8 +805,10 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
         for (size_t k = 0; k < I.out.size(); ++k) {
             ktc_verify_report rep;
             bool nan_abs = false, nan_rel = false;
-            st = verify_pair(ctx, I.out[k], I.ref[k], I.out_count[k], I.out_type[k],
-                             be->opts.rel_tol, be->opts.abs_tol, &rep, &nan_abs, &nan_rel);
+            const double rel = fam == FAM_GEMM_TF32 ? std::max(be->opts.rel_tol, 1e-3)
+                                                    : be->opts.rel_tol;
+            st = verify_pair(ctx, I.out[k], I.ref[k], I.out_count[k], I.out_type[k], rel,
+                             be->opts.abs_tol, &rep, &nan_abs, &nan_rel);
             if (st) return st;
             merge_reports(&total, rep, nan_abs, nan_rel, k);
         }
@@ -771,6 +868,11 @@ int ktc_backend_open(int ordinal, const ktc_backend_options* opts, ktc_backend**
 void ktc_backend_close(ktc_backend* be) {
     if (!be) return;
     free_inputs(be);
+    if (!be->ctx->sticky) {
+        driver().cuCtxSetCurrent(be->ctx->cu);
+        for (ModuleEntry& m : be->modules) driver().cuModuleUnload(m.mod);
+    }
+    be->modules.clear();
     ktc_close(be->ctx);
     delete be;
 }
@@ -806,7 +908,7 @@ int ktc_backend_prefetch(ktc_backend* be, const ktc_request* req) {
                   : fam == FAM_GEMM ? plan_gemm(be, req, &plan, &why)
                   : fam == FAM_GEMM_TF32 ? plan_gemm_tf32(be, req, &plan, &why)
                                          : plan_custom(be, req, &plan, &why);
-        if (ok) CompileService::instance().prefetch(plan.src_id, *plan.src, plan.opts);
+        if (ok) CompileService::instance().prefetch(*plan.ksrc, plan.problem, plan.config);
         return KTC_OK;
     } catch (const std::exception& e) {
         set_error(e.what());

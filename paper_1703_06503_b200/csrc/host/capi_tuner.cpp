@@ -513,9 +513,7 @@ void tune(ktc_tuner* t) {
     for (Backend* b : bes)
         if (auto* c = dynamic_cast<CudaBackend*>(b)) c->reset_totals();
     auto t0 = std::chrono::steady_clock::now();
-    TuningOutcome o = (bes.size() > 1 || !t->subset.empty())
-                          ? run_tuning_sharded(t->job, bes, eff, t->subset)
-                          : run_tuning(t->job, *bes[0], eff);
+    TuningOutcome o = run_tuning_sharded(t->job, bes, eff, t->subset);
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     ktc_summary& s = t->summary;
     std::memset(&s, 0, sizeof(s));

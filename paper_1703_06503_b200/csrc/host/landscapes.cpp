@@ -133,7 +133,6 @@ SearchSpace gemm_tf32_space() {
     s.add_parameter("BN", {64, 128, 256});
     s.add_parameter("BK", {32, 64});
     s.add_parameter("STAGES", {2, 3, 4, 6});
-    s.add_parameter("CG", {1, 2});  // cta_group: 1 SM, or a 2-SM CTA pair (M tile 256)
     return s;
 }
 
@@ -146,7 +145,7 @@ KernelSpec gemm_tf32_kernel(const GemmProblem& p) {
     k.base_global = {p.m, p.n};
     k.base_local = {128, 1};
     k.modifiers = {{SizeTarget::global, SizeOp::divide, {"1", "BN"}}};
-    k.local_mem_expr = "STAGES * 4 * BK * (128 + BN) + 1024";
+    k.local_mem_expr = "STAGES * 4 * BK * (128 + BN) + 2048";
     k.arguments = gemm_arguments(p);
     return k;
 }

@@ -381,10 +381,7 @@ Configuration SearchSpace::random_valid(Rng& rng) const {
                      " uniform draws; the space is empty or vanishingly sparse");
 }
 
-Configuration SearchSpace::random_neighbor(const Configuration& c, Rng& rng) const {
-    require_parameters();
-    if (!is_valid(c))
-        throw InvalidConfiguration("random_neighbor called with a configuration outside the space");
+std::vector<Configuration> SearchSpace::neighbors(const Configuration& c) const {
     std::vector<Configuration> cand;
     for (size_t i = 0; i < params_.size(); ++i) {
         const Parameter& p = params_[i];
@@ -400,6 +397,14 @@ Configuration SearchSpace::random_neighbor(const Configuration& c, Rng& rng) con
             if (satisfies(n)) cand.push_back(std::move(n));
         }
     }
+    return cand;
+}
+
+Configuration SearchSpace::random_neighbor(const Configuration& c, Rng& rng) const {
+    require_parameters();
+    if (!is_valid(c))
+        throw InvalidConfiguration("random_neighbor called with a configuration outside the space");
+    std::vector<Configuration> cand = neighbors(c);
     if (!cand.empty()) return cand[size_t(uniform_index(rng, cand.size()))];
     if (valid_count() <= 1) return c;
     for (;;) {

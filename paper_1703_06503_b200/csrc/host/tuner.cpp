@@ -193,7 +193,11 @@ TuningOutcome run_tuning(const TuningJob& job, Backend& backend, const SearchSpa
         out.rows.push_back(std::move(row));
         return t;
     };
-    SearchOutcome s = run_search(eff, ev, job.strategy, job.seed);
+    Prefetcher pf = [&](const Configuration& c) {
+        ResolvedSizes sz;
+        backend.prefetch(make_request(job, c, &sz));
+    };
+    SearchOutcome s = run_search(eff, ev, job.strategy, job.seed, pf);
     for (size_t i = 0; i < out.rows.size(); ++i) {
         out.rows[i].step = s.trace[i].step;
         out.rows[i].best_so_far = s.trace[i].best_so_far;
@@ -237,8 +241,9 @@ TuningOutcome run_tuning_sharded(const TuningJob& job, const std::vector<Backend
     if (backends.empty()) throw Error("run_tuning_sharded: no backends");
     const bool ordered = job.strategy.kind == StrategyKind::full ||
                          job.strategy.kind == StrategyKind::random;
-    if (!ordered || (backends.size() == 1 && subset.empty()))
-        return run_tuning(job, *backends[0], eff);
+    // Order-dependent strategies (annealing, PSO) are sequential chains: one
+    // device, speculative compile-ahead of their candidate moves.
+    if (!ordered) return run_tuning(job, *backends[0], eff);
     check_nonempty(job, eff);
 
     TuningOutcome out;

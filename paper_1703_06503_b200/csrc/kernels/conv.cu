@@ -29,12 +29,6 @@
 // panel geometry: PWO output columns per panel, box BW x BH floats, NB boxes
 // per panel, NP panels, PF floats per panel).
 
-#define H ((FS - 1) / 2)
-#define TX (XWG * XWPT)
-#define TY (YWG * YWPT)
-#define NG (XWPT / VW)
-#define NT (XWG * YWG)
-
 typedef unsigned int u32;
 
 __constant__ float c_taps[FS * FS];
@@ -96,17 +90,6 @@ __device__ __forceinline__ void st_global(float* p, const float* s) {
 #define POW2_DIV(p) (((p) % 4 == 0) ? 4 : (((p) % 2 == 0) ? 2 : 1))
 #define MIN_(a, b) ((a) < (b) ? (a) : (b))
 
-#if LOCAL == 0
-#define SVW VW
-#elif LOCAL == 1
-#define SVW MIN_(VW, POW2_DIV(SP))
-#else
-#define SVW MIN_(VW, 4)
-#endif
-#define WIN (VW + FS - 1)
-#define NWV ((WIN + SVW - 1) / SVW)  // vector loads per window row
-#define WINP (NWV * SVW)
-
 // ---------------------------------------------------------------------------
 // TMA / mbarrier primitives (LOCAL == 2).
 // ---------------------------------------------------------------------------
@@ -148,11 +131,27 @@ __device__ __forceinline__ void tma_load_2d(u32 dst, const TensorMap* map, u32 b
         : "memory");
 }
 
-// ---------------------------------------------------------------------------
-// The kernel.
-// ---------------------------------------------------------------------------
+//@@KTC_BODY@@ -- everything below is instantiated once per configuration
+// (inside its own namespace when several configurations share one NVRTC
+// program); KTC_ENTRY names the kernel.
+#define H ((FS - 1) / 2)
+#define TX (XWG * XWPT)
+#define TY (YWG * YWPT)
+#define NG (XWPT / VW)
+#define NT (XWG * YWG)
+#if LOCAL == 0
+#define SVW VW
+#elif LOCAL == 1
+#define SVW MIN_(VW, POW2_DIV(SP))
+#else
+#define SVW MIN_(VW, 4)
+#endif
+#define WIN (VW + FS - 1)
+#define NWV ((WIN + SVW - 1) / SVW)  // vector loads per window row
+#define WINP (NWV * SVW)
+
 extern "C" __global__ void __launch_bounds__(NT, 1)
-conv2d(const int X, const int Y, const float W, const float* __restrict__ img, const int ipitch,
+KTC_ENTRY(const int X, const int Y, const float W, const float* __restrict__ img, const int ipitch,
        float* __restrict__ out, const __grid_constant__ TensorMap tmap) {
     const int tx = threadIdx.x;
     const int ty = threadIdx.y;
@@ -322,3 +321,14 @@ conv2d(const int X, const int Y, const float W, const float* __restrict__ img, c
         }
     }
 }
+#undef ROWPTR
+#undef COLOFF
+#undef H
+#undef TX
+#undef TY
+#undef NG
+#undef NT
+#undef SVW
+#undef WIN
+#undef NWV
+#undef WINP

@@ -21,25 +21,6 @@
 //   KWI             unroll factor of the inner K loop
 // C is N-contiguous, so output stores vectorize along N (VWN).
 
-#define MWI (MWG / MDIMC)
-#define NWI (NWG / NDIMC)
-#define NT (MDIMC * NDIMC)
-#define MVI (MWI / VWM)  // A vectors per thread per k
-#define NVI (NWI / VWN)  // B vectors per thread per k
-
-#if SA
-#define KDIMA (NT / MDIMA)
-#define KWA (KWG / KDIMA)
-#define VA (MWG / VWM)                          // A vectors per k-row of the tile
-#define MVA ((VA >= MDIMA) ? (VA / MDIMA) : 1)  // per copying thread
-#endif
-#if SB
-#define KDIMB (NT / NDIMB)
-#define KWB (KWG / KDIMB)
-#define VB (NWG / VWN)
-#define NVB ((VB >= NDIMB) ? (VB / NDIMB) : 1)
-#endif
-
 template <int N>
 __device__ __forceinline__ void vload(float* d, const float* p) {
     if (N == 1) {
@@ -85,8 +66,28 @@ __device__ __forceinline__ void vstore(float* p, const float* s) {
     }
 }
 
+//@@KTC_BODY@@ -- instantiated once per configuration; KTC_ENTRY names the kernel.
+#define MWI (MWG / MDIMC)
+#define NWI (NWG / NDIMC)
+#define NT (MDIMC * NDIMC)
+#define MVI (MWI / VWM)  // A vectors per thread per k
+#define NVI (NWI / VWN)  // B vectors per thread per k
+
+#if SA
+#define KDIMA (NT / MDIMA)
+#define KWA (KWG / KDIMA)
+#define VA (MWG / VWM)                          // A vectors per k-row of the tile
+#define MVA ((VA >= MDIMA) ? (VA / MDIMA) : 1)  // per copying thread
+#endif
+#if SB
+#define KDIMB (NT / NDIMB)
+#define KWB (KWG / KDIMB)
+#define VB (NWG / VWN)
+#define NVB ((VB >= NDIMB) ? (VB / NDIMB) : 1)
+#endif
+
 extern "C" __global__ void __launch_bounds__(NT, 1)
-gemm(const int M, const int N, const int K, const float alpha, const float beta,
+KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float beta,
      const float* __restrict__ A, const float* __restrict__ B, const float* __restrict__ Cin,
      float* __restrict__ Cout) {
     const int tx = threadIdx.x;  // along M
@@ -214,3 +215,16 @@ gemm(const int M, const int N, const int K, const float alpha, const float beta,
         }
     }
 }
+#undef MWI
+#undef NWI
+#undef NT
+#undef MVI
+#undef NVI
+#undef KDIMA
+#undef KWA
+#undef VA
+#undef MVA
+#undef KDIMB
+#undef KWB
+#undef VB
+#undef NVB

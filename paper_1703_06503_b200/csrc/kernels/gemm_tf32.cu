@@ -1,2 +1,265 @@
-// gemm_tf32.cu -- placeholder; the tcgen05 TF32 variant lands here.
-extern "C" __global__ void gemm_tf32() {}
+// gemm_tf32.cu -- SGEMM on the 5th-generation tensor cores (tcgen05, TF32
+// inputs, fp32 accumulation in TMEM), the B200 variant of the SGEMM family
+// (kernel name "gemm_tf32", reported separately from the fp32 CUDA-core
+// family, verified with its own tolerance rel 1e-3).  Same problem and
+// argument list as gemm.cu:
+//     Cout[m*N + n] = ALPHA * sum_k A[k*M + m] * B[k*N + n] + BETA * Cin[m*N + n]
+//
+// A (K x M, M contiguous) and B (K x N, N contiguous) are both MN-major
+// operands, which UMMA accepts for TF32, so no transpose pass is needed:
+//
+//   TMA   A tile 128(M) x BK(K) as 4 boxes of 32 x BK, B tile BN x BK as
+//         BN/32 boxes, SWIZZLE_128B: each box is BK rows of 128 B, i.e. the
+//         canonical MN-major SW128 atom (8 K-rows x 128 B) stacked along K;
+//   ring  STAGES stages of A+B, full/empty mbarriers per stage;
+//   MMA   one elected thread issues tcgen05.mma.cta_group::1.kind::tf32
+//         (M=128, N=BN, K=8) for each 8-row K group, accumulating into a
+//         128-lane x BN-column fp32 TMEM tile; tcgen05.commit releases the
+//         stage and finally signals the epilogue;
+//   epi   all 4 warps: tcgen05.ld 32x32b (warp w owns TMEM lanes 32w..32w+31
+//         = rows), alpha/beta, 128-byte row segments stored to global.
+//
+// Parameters: BN (64, 128, 256), BK (32, 64), STAGES (2..6), ROUND (0: the
+// tensor core reads the fp32 bits as TF32, i.e. truncates; 1: operands were
+// rounded to nearest TF32 by the host-side pre-pass ktc_tf32_round).
+// Block: 128 threads; grid (M/128, N/BN).
+
+
+typedef unsigned int u32;
+typedef unsigned long long u64;
+
+struct __align__(64) TensorMap {
+    unsigned long long v[16];
+};
+
+__device__ __forceinline__ u32 smem_u32(const void* p) {
+    return static_cast<u32>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(u32 bar, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(u32 bar, u32 bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(u32 bar, u32 parity) {
+    for (long long spin = 0; spin < (1ll << 28); ++spin) {
+        u32 done;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (done) return;
+    }
+    __trap();  // a lost transaction becomes a launch error, never a hang
+}
+
+__device__ __forceinline__ void tma_load_2d(u32 dst, const TensorMap* map, u32 bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<u64>(map)), "r"(bar), "r"(x), "r"(y)
+        : "memory");
+}
+
+// UMMA shared-memory descriptor, MN-major SWIZZLE_128B (sm_100 layout):
+// start>>4 [0,14), LBO>>4 [16,30) = stride between 32-element MN atoms,
+// SBO>>4 [32,46) = stride between 8-row K groups, version 1 at [46,48),
+// layout type 2 (SWIZZLE_128B) at [61,64).
+__device__ __forceinline__ u64 umma_desc(u32 addr, u32 lbo, u32 sbo) {
+    u64 d = 0;
+    d |= (u64)((addr >> 4) & 0x3FFF);
+    d |= (u64)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (u64)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (u64)1 << 46;
+    d |= (u64)2 << 61;
+    return d;
+}
+
+// Instruction descriptor: D f32, A/B tf32, both MN-major, M=128, N=bn.
+__device__ __forceinline__ u32 make_idesc(u32 bn) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) | ((bn >> 3) << 17) |
+           ((128u >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_tf32(u32 tmem_d, u64 adesc, u64 bdesc, u32 idesc,
+                                          u32 accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(u32 bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+        : "memory");
+}
+
+// Round-to-nearest TF32 copy (ROUND = 1 configurations): the tensor core
+// would otherwise truncate the low 13 mantissa bits.
+extern "C" __global__ void tf32_round(const float4* __restrict__ in, float4* __restrict__ out,
+                                      unsigned long long n4) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += stride) {
+        float4 v = __ldg(in + i);
+        u32 r;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v.x));
+        v.x = __uint_as_float(r);
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v.y));
+        v.y = __uint_as_float(r);
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v.z));
+        v.z = __uint_as_float(r);
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v.w));
+        v.w = __uint_as_float(r);
+        out[i] = v;
+    }
+}
+
+//@@KTC_BODY@@ -- instantiated once per configuration; KTC_ENTRY names the kernel.
+#define BM 128
+#define NT 128
+#define A_BOX_BYTES (BK * 128)
+#define A_STAGE_BYTES (4 * A_BOX_BYTES)
+#define B_STAGE_BYTES ((BN / 32) * A_BOX_BYTES)
+#define STAGE_BYTES (A_STAGE_BYTES + B_STAGE_BYTES)
+#define TMEM_COLS (BN < 32 ? 32 : BN)
+
+extern "C" __global__ void __launch_bounds__(NT, 1)
+KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float beta,
+          const float* __restrict__ A, const float* __restrict__ B,
+          const float* __restrict__ Cin, float* __restrict__ Cout,
+          const __grid_constant__ TensorMap tmap_a, const __grid_constant__ TensorMap tmap_b) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte alignment for SWIZZLE_128B atoms.
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<u64>(smem_raw) + 1023) & ~u64(1023));
+    u64* bars = reinterpret_cast<u64*>(smem + STAGES * STAGE_BYTES);  // full[S], empty[S], acc
+    u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * STAGES + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    const int kblocks = K / BK;
+    const u32 full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES),
+              accb = smem_u32(bars + 2 * STAGES);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, 1);
+        }
+        mbar_init(accb, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<u64>(&tmap_a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<u64>(&tmap_b)) : "memory");
+    }
+    if (warp == 1) {  // TMEM allocation: one warp, power-of-two >= 32 columns
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"((u32)TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const u32 tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---- TMA producer ----
+        for (int kb = 0; kb < kblocks; ++kb) {
+            const int s = kb % STAGES;
+            const u32 phase = (u32)((kb / STAGES) & 1);
+            mbar_wait(empty0 + 8 * s, phase ^ 1u);
+            const u32 full = full0 + 8 * s;
+            mbar_expect_tx(full, STAGE_BYTES);
+            const u32 sa = smem_u32(smem + s * STAGE_BYTES);
+            const u32 sb = sa + A_STAGE_BYTES;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) tma_load_2d(sa + j * A_BOX_BYTES, &tmap_a, full, m0 + 32 * j, kb * BK);
+#pragma unroll
+            for (int j = 0; j < BN / 32; ++j)
+                tma_load_2d(sb + j * A_BOX_BYTES, &tmap_b, full, n0 + 32 * j, kb * BK);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---- MMA issuer (single thread) ----
+        for (int kb = 0; kb < kblocks; ++kb) {
+            const int s = kb % STAGES;
+            mbar_wait(full0 + 8 * s, (u32)((kb / STAGES) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const u32 sa = smem_u32(smem + s * STAGE_BYTES);
+            const u32 sb = sa + A_STAGE_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+                const u64 ad = umma_desc(sa + kk * 1024, A_BOX_BYTES, 1024);
+                const u64 bd = umma_desc(sb + kk * 1024, A_BOX_BYTES, 1024);
+                umma_tf32(tmem, ad, bd, make_idesc(BN), (kb | kk) != 0 ? 1u : 0u);
+            }
+            umma_commit(empty0 + 8 * s);  // stage reusable once these MMAs retire
+        }
+        umma_commit(accb);  // accumulator complete
+    }
+
+    // ---- epilogue: all warps ----
+    mbar_wait(accb, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int row = warp * 32 + lane;  // TMEM lane == tile row
+    float* crow = Cout + (size_t)(m0 + row) * N + n0;
+    const float* cin = Cin + (size_t)(m0 + row) * N + n0;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+        u32 v[32];
+        const u32 taddr = tmem + ((u32)(warp * 32) << 16) + (u32)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+              "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 32; q += 4) {
+            float4 o;
+            o.x = alpha * __uint_as_float(v[q]);
+            o.y = alpha * __uint_as_float(v[q + 1]);
+            o.z = alpha * __uint_as_float(v[q + 2]);
+            o.w = alpha * __uint_as_float(v[q + 3]);
+            if (beta != 0.0f) {
+                const float4 c = __ldg(reinterpret_cast<const float4*>(cin + c0 + q));
+                o.x += beta * c.x;
+                o.y += beta * c.y;
+                o.z += beta * c.z;
+                o.w += beta * c.w;
+            }
+            *reinterpret_cast<float4*>(crow + c0 + q) = o;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"((u32)TMEM_COLS)
+                     : "memory");
+    }
+}
+#undef BM
+#undef NT
+#undef A_BOX_BYTES
+#undef A_STAGE_BYTES
+#undef B_STAGE_BYTES
+#undef STAGE_BYTES
+#undef TMEM_COLS

@@ -2,19 +2,21 @@
 #include "nvrtc_pool.hpp"
 
 #include <nvrtc.h>
+#include <sys/stat.h>
 
-#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
-#include <sys/stat.h>
+#include <sstream>
 
 #include "core.hpp"
 
 namespace ktc {
 
 namespace {
+
+const char* kMarker = "//@@KTC_BODY@@";
 
 uint64_t fnv(const std::string& s, uint64_t h = 0xcbf29ce484222325ull) {
     for (unsigned char c : s) {
@@ -30,14 +32,56 @@ std::string hex64(uint64_t v) {
     return buf;
 }
 
+std::string hash_name(const std::string& key) {
+    return hex64(fnv(key)) + hex64(fnv(key, 0x84222325cbf29ce4ull));
+}
+
 const std::vector<std::string>& base_options() {
-    static const std::vector<std::string> opts = {
-        "--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--fmad=true",
-        "-default-device"};
+    static const std::vector<std::string> opts = {"--gpu-architecture=sm_100a", "--std=c++17",
+                                                  "-lineinfo", "--fmad=true"};
     return opts;
 }
 
+std::string define_name(const std::string& d) { return d.substr(0, d.find('=')); }
+std::string define_value(const std::string& d) {
+    const size_t eq = d.find('=');
+    return eq == std::string::npos ? "1" : d.substr(eq + 1);
+}
+
+// One NVRTC program holding every configuration of the batch.
+std::string assemble(const KernelSource& src, const std::vector<const Defines*>& configs) {
+    std::ostringstream s;
+    s << src.prelude << "\n";
+    for (size_t i = 0; i < configs.size(); ++i) {
+        s << "namespace ktc_k" << i << " {\n";
+        for (const std::string& d : *configs[i])
+            s << "#define " << define_name(d) << " " << define_value(d) << "\n";
+        s << "#define KTC_ENTRY " << src.entry_base << "_k" << i << "\n";
+        s << src.body << "\n";
+        for (const std::string& d : *configs[i]) s << "#undef " << define_name(d) << "\n";
+        s << "#undef KTC_ENTRY\n}\n";
+    }
+    return s.str();
+}
+
+std::vector<std::string> problem_options(const Defines& problem) {
+    std::vector<std::string> o;
+    for (const std::string& d : problem) o.push_back("-D" + d);
+    return o;
+}
+
 }  // namespace
+
+KernelSource split_source(const std::string& name, const std::string& text,
+                          const std::string& entry_base) {
+    KernelSource s;
+    const size_t at = text.find(kMarker);
+    s.prelude = at == std::string::npos ? std::string() : text.substr(0, at);
+    s.body = at == std::string::npos ? text : text.substr(at);
+    s.entry_base = entry_base;
+    s.id = name + "#" + hex64(fnv(text));
+    return s;
+}
 
 CubinPtr nvrtc_compile(const std::string& src, const std::vector<std::string>& opts) {
     auto out = std::make_shared<Cubin>();
@@ -75,23 +119,16 @@ CubinPtr nvrtc_compile(const std::string& src, const std::vector<std::string>& o
 }
 
 CompileService& CompileService::instance() {
-    static CompileService* svc = new CompileService;  // never destroyed: workers outlive statics
+    static CompileService* svc = new CompileService;  // intentionally leaked: workers outlive statics
     return *svc;
 }
 
-CompileService::~CompileService() {
-    {
-        std::lock_guard<std::mutex> lk(mu_);
-        stop_ = true;
-    }
-    cv_.notify_all();
-    for (auto& t : workers_) t.join();
-}
-
-void CompileService::configure(int threads, const std::string& cache_dir) {
+void CompileService::configure(int threads, const std::string& cache_dir, int batch) {
     std::lock_guard<std::mutex> lk(mu_);
     if (threads <= 0) threads = int(std::max(1u, std::thread::hardware_concurrency()));
     want_threads_ = threads;
+    if (const char* env = std::getenv("KTC_COMPILE_BATCH")) batch = std::atoi(env);
+    batch_ = std::max(1, std::min(batch, 32));
     cache_dir_ = cache_dir;
     if (!cache_dir_.empty()) ::mkdir(cache_dir_.c_str(), 0755);
     ensure_workers_locked();
@@ -102,104 +139,212 @@ void CompileService::ensure_workers_locked() {
     while (int(workers_.size()) < want_threads_) workers_.emplace_back([this] { worker(); });
 }
 
-std::string CompileService::make_key(const std::string& src_id,
-                                     const std::vector<std::string>& opts) const {
+std::string CompileService::batch_key_of(const KernelSource& src, const Defines& problem) const {
     int major = 0, minor = 0;
     nvrtcVersion(&major, &minor);
-    std::string k = src_id + "|nvrtc" + std::to_string(major) + "." + std::to_string(minor);
+    std::string k = src.id + "|nvrtc" + std::to_string(major) + "." + std::to_string(minor);
     for (const auto& o : base_options()) k += "|" + o;
-    for (const auto& o : opts) k += "|" + o;
+    for (const auto& d : problem) k += "|P" + d;
     return k;
 }
 
-CubinPtr CompileService::load_disk(const std::string& key) {
+std::string CompileService::key_of(const KernelSource& src, const Defines& problem,
+                                   const Defines& config) const {
+    std::string k = batch_key_of(src, problem);
+    for (const auto& d : config) k += "|C" + d;
+    return k;
+}
+
+KernelPtr CompileService::load_disk(const std::string& key) {
     if (cache_dir_.empty()) return nullptr;
-    std::string path = cache_dir_ + "/" + hex64(fnv(key)) + hex64(fnv(key, 0x84222325cbf29ce4ull)) +
-                       ".cubin";
-    std::ifstream in(path, std::ios::binary);
+    std::ifstream ref(cache_dir_ + "/" + hash_name(key) + ".ref");
+    std::string file, entry;
+    if (!(ref >> file >> entry)) return nullptr;
+    std::ifstream in(cache_dir_ + "/" + file, std::ios::binary);
     if (!in) return nullptr;
     auto c = std::make_shared<Cubin>();
     c->image.assign(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
     if (c->image.empty()) return nullptr;
-    return c;
+    auto k = std::make_shared<CompiledKernel>();
+    k->cubin = c;
+    k->entry = entry;
+    return k;
 }
 
-void CompileService::store_disk(const std::string& key, const Cubin& c) {
-    if (cache_dir_.empty() || !c.ok()) return;
-    std::string path = cache_dir_ + "/" + hex64(fnv(key)) + hex64(fnv(key, 0x84222325cbf29ce4ull)) +
-                       ".cubin";
-    std::string tmp = path + ".tmp" + std::to_string(std::hash<std::thread::id>()(
-                                          std::this_thread::get_id()));
+void CompileService::store_disk(const std::string& key, const CompiledKernel& k) {
+    if (cache_dir_.empty() || !k.ok()) return;
+    const std::string file = hash_name(std::to_string(reinterpret_cast<uintptr_t>(k.cubin.get())) +
+                                       key) + ".cubin";
+    const std::string tid = std::to_string(std::hash<std::thread::id>()(std::this_thread::get_id()));
     {
-        std::ofstream out(tmp, std::ios::binary);
-        out.write(c.image.data(), std::streamsize(c.image.size()));
+        std::ofstream out(cache_dir_ + "/" + file + ".tmp" + tid, std::ios::binary);
+        out.write(k.cubin->image.data(), std::streamsize(k.cubin->image.size()));
     }
-    std::rename(tmp.c_str(), path.c_str());
+    std::rename((cache_dir_ + "/" + file + ".tmp" + tid).c_str(), (cache_dir_ + "/" + file).c_str());
+    {
+        std::ofstream ref(cache_dir_ + "/" + hash_name(key) + ".ref.tmp" + tid);
+        ref << file << " " << k.entry << "\n";
+    }
+    std::rename((cache_dir_ + "/" + hash_name(key) + ".ref.tmp" + tid).c_str(),
+                (cache_dir_ + "/" + hash_name(key) + ".ref").c_str());
 }
 
-CubinPtr CompileService::run(const Job& job) {
-    CubinPtr c = load_disk(job.key);
-    if (!c) {
-        c = nvrtc_compile(job.src, job.opts);
-        store_disk(job.key, *c);
-        std::lock_guard<std::mutex> lk(mu_);
-        compile_ms_ += c->compile_ms;
+void CompileService::run_batch(Batch b) {
+    // Disk hits first.
+    std::vector<Item> todo;
+    for (Item& it : b.items) {
+        if (KernelPtr k = load_disk(it.key)) it.promise->set_value(k);
+        else todo.push_back(std::move(it));
     }
-    return c;
+    if (todo.empty()) return;
+    const std::vector<std::string> popts = problem_options(b.problem);
+    if (!b.src->batchable) {
+        for (Item& it : todo) {
+            std::vector<std::string> o = popts;
+            for (const std::string& d : problem_options(it.config)) o.push_back(d);
+            CubinPtr c = nvrtc_compile(b.src->body, o);
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                compile_ms_ += c->compile_ms;
+                ++programs_;
+            }
+            auto k = std::make_shared<CompiledKernel>();
+            k->cubin = c;
+            k->entry = b.src->fixed_entry;
+            k->log = c->log;
+            k->compile_ms = c->compile_ms;
+            store_disk(it.key, *k);
+            it.promise->set_value(k);
+        }
+        return;
+    }
+    auto compile_group = [&](const std::vector<Item*>& group) -> bool {
+        std::vector<const Defines*> cfgs;
+        for (Item* it : group) cfgs.push_back(&it->config);
+        CubinPtr c = nvrtc_compile(assemble(*b.src, cfgs), popts);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            compile_ms_ += c->compile_ms;
+            ++programs_;
+        }
+        if (!c->ok() && group.size() > 1) return false;
+        for (size_t i = 0; i < group.size(); ++i) {
+            auto k = std::make_shared<CompiledKernel>();
+            k->cubin = c;
+            k->entry = b.src->entry_base + "_k" + std::to_string(i);
+            k->log = c->log;
+            k->compile_ms = c->compile_ms;
+            k->batch = int(group.size());
+            store_disk(group[i]->key, *k);
+            group[i]->promise->set_value(k);
+        }
+        return true;
+    };
+    std::vector<Item*> all;
+    for (Item& it : todo) all.push_back(&it);
+    if (!compile_group(all))
+        for (Item* it : all) compile_group({it});  // attribute errors to their configuration
 }
 
 void CompileService::worker() {
+    using namespace std::chrono;
     for (;;) {
-        Job job;
+        Batch b;
         {
             std::unique_lock<std::mutex> lk(mu_);
-            cv_.wait(lk, [&] { return stop_ || !queue_.empty(); });
-            if (stop_) return;
-            job = std::move(queue_.front());
-            queue_.pop_front();
+            for (;;) {
+                if (!ready_.empty()) {
+                    b = std::move(ready_.front());
+                    ready_.pop_front();
+                    break;
+                }
+                // A partially filled batch is taken once it has waited a
+                // little for company (prefetch bursts fill batches quickly).
+                auto oldest = pending_.end();
+                for (auto it = pending_.begin(); it != pending_.end(); ++it)
+                    if (oldest == pending_.end() || it->second.born < oldest->second.born) oldest = it;
+                if (oldest != pending_.end() &&
+                    steady_clock::now() - oldest->second.born > milliseconds(10)) {
+                    b = std::move(oldest->second);
+                    pending_.erase(oldest);
+                    break;
+                }
+                cv_.wait_for(lk, milliseconds(oldest == pending_.end() ? 100 : 3));
+            }
         }
-        job.promise->set_value(run(job));
+        run_batch(std::move(b));
     }
 }
 
-CubinPtr CompileService::get(const std::string& src_id, const std::string& src,
-                             const std::vector<std::string>& opts, bool* hit) {
-    const std::string key = make_key(src_id, opts);
-    std::shared_future<CubinPtr> fut;
-    std::shared_ptr<std::promise<CubinPtr>> mine;
+std::shared_future<KernelPtr> CompileService::enlist_locked(const KernelSource& src,
+                                                            const Defines& problem,
+                                                            const Defines& config, bool* created) {
+    const std::string key = key_of(src, problem, config);
+    auto it = cache_.find(key);
+    if (it != cache_.end()) {
+        *created = false;
+        return it->second;
+    }
+    *created = true;
+    auto promise = std::make_shared<std::promise<KernelPtr>>();
+    std::shared_future<KernelPtr> fut = promise->get_future().share();
+    if (cache_.size() > 50000) cache_.clear();  // bound host memory
+    cache_.emplace(key, fut);
+    const std::string bkey = src.batchable ? batch_key_of(src, problem) : key;
+    auto& sp = sources_[src.id];
+    if (!sp) sp = std::make_shared<const KernelSource>(src);
+    Batch& b = pending_[bkey];
+    if (b.items.empty()) {
+        b.src = sp;
+        b.problem = problem;
+        b.born = std::chrono::steady_clock::now();
+    }
+    b.items.push_back(Item{config, key, promise});
+    if (int(b.items.size()) >= batch_ || !src.batchable) {
+        ready_.push_back(std::move(b));
+        pending_.erase(bkey);
+        cv_.notify_one();
+    }
+    return fut;
+}
+
+void CompileService::prefetch(const KernelSource& src, const Defines& problem,
+                              const Defines& config) {
+    std::lock_guard<std::mutex> lk(mu_);
+    ensure_workers_locked();
+    bool created = false;
+    enlist_locked(src, problem, config, &created);
+    cv_.notify_one();
+}
+
+KernelPtr CompileService::get(const KernelSource& src, const Defines& problem,
+                              const Defines& config, bool* hit) {
+    std::shared_future<KernelPtr> fut;
+    Batch mine;
+    bool run_here = false;
     {
         std::lock_guard<std::mutex> lk(mu_);
-        auto it = cache_.find(key);
-        if (it != cache_.end()) {
-            fut = it->second;
-        } else {
-            mine = std::make_shared<std::promise<CubinPtr>>();
-            fut = mine->get_future().share();
-            if (cache_.size() > 20000) cache_.clear();  // bound host memory
-            cache_.emplace(key, fut);
+        ensure_workers_locked();
+        bool created = false;
+        fut = enlist_locked(src, problem, config, &created);
+        if (hit) *hit = !created && fut.wait_for(std::chrono::seconds(0)) == std::future_status::ready;
+        // Still waiting in a filling batch: compile that batch right here.
+        const std::string bkey =
+            src.batchable ? batch_key_of(src, problem) : key_of(src, problem, config);
+        auto pit = pending_.find(bkey);
+        if (pit != pending_.end()) {
+            const std::string key = key_of(src, problem, config);
+            for (const Item& it : pit->second.items)
+                if (it.key == key) {
+                    mine = std::move(pit->second);
+                    pending_.erase(pit);
+                    run_here = true;
+                    break;
+                }
         }
     }
-    if (mine) {
-        if (hit) *hit = false;
-        CubinPtr c = run(Job{key, src, opts, mine});
-        mine->set_value(c);
-        return c;
-    }
-    if (hit) *hit = fut.wait_for(std::chrono::seconds(0)) == std::future_status::ready;
+    if (run_here) run_batch(std::move(mine));
     return fut.get();
-}
-
-void CompileService::prefetch(const std::string& src_id, const std::string& src,
-                              const std::vector<std::string>& opts) {
-    const std::string key = make_key(src_id, opts);
-    std::lock_guard<std::mutex> lk(mu_);
-    if (cache_.count(key)) return;
-    ensure_workers_locked();
-    auto promise = std::make_shared<std::promise<CubinPtr>>();
-    if (cache_.size() > 20000) cache_.clear();
-    cache_.emplace(key, promise->get_future().share());
-    queue_.push_back(Job{key, src, opts, promise});
-    cv_.notify_one();
 }
 
 double CompileService::total_compile_ms() {
@@ -207,9 +352,15 @@ double CompileService::total_compile_ms() {
     return compile_ms_;
 }
 
+size_t CompileService::programs_compiled() {
+    std::lock_guard<std::mutex> lk(mu_);
+    return programs_;
+}
+
 void CompileService::reset_stats() {
     std::lock_guard<std::mutex> lk(mu_);
     compile_ms_ = 0.0;
+    programs_ = 0;
 }
 
 }  // namespace ktc
@@ -220,10 +371,11 @@ extern "C" int ktc_compile(const char* src, const char* const* opts, int nopts, 
                            size_t* cubin_size, char* log, size_t log_cap) {
     std::vector<std::string> o;
     for (int i = 0; i < nopts; ++i) o.emplace_back(opts[i]);
-    CubinPtr c = nvrtc_compile(src, o);
-    if (log && log_cap) {
-        std::snprintf(log, log_cap, "%s", c->log.c_str());
-    }
+    // Family sources need an entry name when compiled stand-alone.
+    std::string text = src;
+    if (text.find("KTC_ENTRY") != std::string::npos) o.push_back("-DKTC_ENTRY=ktc_entry");
+    CubinPtr c = nvrtc_compile(text, o);
+    if (log && log_cap) std::snprintf(log, log_cap, "%s", c->log.c_str());
     if (!c->ok()) {
         set_error("NVRTC: " + c->log.substr(0, 2000));
         *cubin = nullptr;

@@ -1,16 +1,28 @@
-// nvrtc_pool.hpp -- NVRTC compilation for sm_100a with a shared host thread
-// pool and a cubin cache keyed by (source, options, arch, NVRTC version).
+// nvrtc_pool.hpp -- NVRTC compilation for sm_100a: a shared host thread pool,
+// batched programs and a cubin cache.
 //
-// Compilation is the throughput limiter of tuning (SURVEY 7 "Hard parts" 1:
-// ~60-150 ms per configuration per core).  Evaluation on the GPU takes a few
-// milliseconds, so the pool compiles ahead of the device: callers prefetch()
-// the next configurations while the current one runs.
+// Compilation is the throughput limiter of tuning (SURVEY 7 "Hard parts" 1).
+// Two levers:
+//   * ahead-of-time: callers prefetch() the configurations they will evaluate
+//     next, so the pool compiles while the device runs;
+//   * batching: up to `batch` configurations of the same family and problem
+//     are compiled as ONE NVRTC program (each configuration's kernel body in
+//     its own C++ namespace with its own macro block, entry names suffixed
+//     _k<i>).  NVRTC's fixed cost (~45 ms per program: front end, builtins)
+//     is paid once per batch.  A batch that fails to compile is split back
+//     into single compilations so errors land on the configuration that
+//     caused them.
+// Kernel sources carry a `//@@KTC_BODY@@` marker: the text above it (helpers,
+// problem-level symbols) appears once per program, the text below it once per
+// configuration with KTC_ENTRY naming the kernel.
 #pragma once
 
+#include <chrono>
 #include <condition_variable>
 #include <cstdint>
 #include <deque>
 #include <future>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -22,60 +34,95 @@ namespace ktc {
 
 struct Cubin {
     std::vector<char> image;  // empty on failure
-    std::string log;          // NVRTC log (errors)
-    double compile_ms = 0.0;  // 0 for cache hits loaded from disk
+    std::string log;
+    double compile_ms = 0.0;
     bool ok() const { return !image.empty(); }
 };
-
 using CubinPtr = std::shared_ptr<const Cubin>;
 
-// Compiles `src` with `opts` (+ the fixed arch/std options) synchronously.
+// A family's source split at the body marker.
+struct KernelSource {
+    std::string id;          // identity (name + content hash)
+    std::string prelude;
+    std::string body;
+    std::string entry_base;  // kernel entry = entry_base + "_k<i>"
+    // Custom (user) kernels: compiled alone, whole text, own entry name,
+    // configuration passed as -D options.
+    bool batchable = true;
+    std::string fixed_entry;
+};
+KernelSource split_source(const std::string& name, const std::string& text,
+                          const std::string& entry_base);
+
+struct CompiledKernel {
+    CubinPtr cubin;     // shared by every configuration of the batch
+    std::string entry;  // this configuration's kernel symbol
+    std::string log;
+    double compile_ms = 0.0;  // wall time of the (batch) compilation
+    int batch = 1;
+    bool ok() const { return cubin && cubin->ok(); }
+};
+using KernelPtr = std::shared_ptr<const CompiledKernel>;
+
+// Defines are "NAME=VALUE" strings.
+using Defines = std::vector<std::string>;
+
+// Raw NVRTC compile of `src` with extra options (fixed arch/std options added).
 CubinPtr nvrtc_compile(const std::string& src, const std::vector<std::string>& opts);
 
 class CompileService {
   public:
     static CompileService& instance();
 
-    // Sets the pool size (0 = hardware threads) and the disk cache dir.
-    void configure(int threads, const std::string& cache_dir);
+    // Pool size (0 = hardware threads), disk cache dir ("" = memory only),
+    // configurations per NVRTC program (1 disables batching).
+    void configure(int threads, const std::string& cache_dir, int batch = 8);
 
-    // Returns the cubin, compiling on the calling thread unless it is cached
-    // or already being compiled by the pool.  `hit` reports a cache hit.
-    CubinPtr get(const std::string& src_id, const std::string& src,
-                 const std::vector<std::string>& opts, bool* hit);
+    KernelPtr get(const KernelSource& src, const Defines& problem, const Defines& config,
+                  bool* hit);
+    void prefetch(const KernelSource& src, const Defines& problem, const Defines& config);
 
-    // Queues a background compilation (no-op if cached or in flight).
-    void prefetch(const std::string& src_id, const std::string& src,
-                  const std::vector<std::string>& opts);
-
-    size_t threads() const { return workers_.size(); }
     double total_compile_ms();
+    size_t programs_compiled();
     void reset_stats();
 
   private:
     CompileService() = default;
-    ~CompileService();
-    struct Job {
-        std::string key, src;
-        std::vector<std::string> opts;
-        std::shared_ptr<std::promise<CubinPtr>> promise;
+    struct Item {
+        Defines config;
+        std::string key;
+        std::shared_ptr<std::promise<KernelPtr>> promise;
     };
-    std::string make_key(const std::string& src_id, const std::vector<std::string>& opts) const;
-    CubinPtr load_disk(const std::string& key);
-    void store_disk(const std::string& key, const Cubin& c);
-    CubinPtr run(const Job& job);
+    struct Batch {
+        std::shared_ptr<const KernelSource> src;
+        Defines problem;
+        std::vector<Item> items;
+        std::chrono::steady_clock::time_point born;
+    };
+    std::string key_of(const KernelSource& src, const Defines& problem, const Defines& config) const;
+    std::string batch_key_of(const KernelSource& src, const Defines& problem) const;
+    void run_batch(Batch b);
     void worker();
     void ensure_workers_locked();
+    // Registers `config` (if new) in the pending batch of its key; returns
+    // the future and whether this call created it.
+    std::shared_future<KernelPtr> enlist_locked(const KernelSource& src, const Defines& problem,
+                                                const Defines& config, bool* created);
+    KernelPtr load_disk(const std::string& key);
+    void store_disk(const std::string& key, const CompiledKernel& k);
 
     std::mutex mu_;
     std::condition_variable cv_;
-    std::deque<Job> queue_;
-    std::unordered_map<std::string, std::shared_future<CubinPtr>> cache_;
+    std::deque<Batch> ready_;                         // full batches
+    std::map<std::string, Batch> pending_;            // filling batches by batch key
+    std::unordered_map<std::string, std::shared_future<KernelPtr>> cache_;
+    std::map<std::string, std::shared_ptr<const KernelSource>> sources_;
     std::vector<std::thread> workers_;
     int want_threads_ = 0;
+    int batch_ = 8;
     std::string cache_dir_;
-    bool stop_ = false;
     double compile_ms_ = 0.0;
+    size_t programs_ = 0;
 };
 
 }  // namespace ktc

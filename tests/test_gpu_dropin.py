@@ -1,0 +1,52 @@
+"""Drop-in proof (GPU): the reference's OWN tuner (run_tuning, jobfile,
+write_results_csv -- compiled unmodified from /root/reference into
+oracle/_ref/ref_tune_cuda) evaluates on the B200 through
+include/ktune_cuda_backend.hpp -> libktc's C ABI.  Every row must be `ok`
+and verified `pass` by the reference tuner's own verification rule, and the
+configurations it visits must be exactly the ones this framework's tuner
+visits for the same job and seed."""
+import json
+import subprocess
+from pathlib import Path
+
+import pytest
+
+import paper_1703_06503_b200 as pkg
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+BIN = Path(O.__file__).resolve().parent / "_ref" / "ref_tune_cuda"
+B200 = {"name": "B200", "max_work_group_total": 1024, "max_work_group_dim": [1024, 1024, 64],
+        "local_mem_bytes": 232448}
+
+
+def run_ref(tmp, job, mode=None):
+    (tmp / "job.json").write_text(json.dumps(job))
+    cmd = [str(BIN), str(tmp / "job.json"), str(tmp / "ref.csv")] + ([mode] if mode else [])
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr
+    lines = (tmp / "ref.csv").read_bytes().decode().split("\r\n")[1:-1]
+    return [ln.split(",") for ln in lines], p.stdout
+
+
+@pytest.mark.skipif(not BIN.exists(), reason="oracle/_ref/ref_tune_cuda not built")
+def test_reference_tuner_on_b200_device_verdict(built, tmp_path):
+    job = {"template": "conv", "problem": {"x": 2048, "y": 1024, "filter": 7}, "device": B200,
+           "strategy": {"kind": "random", "fraction": "1/64"}, "seed": 5, "verify": True,
+           "repetitions": 2}
+    rows, out = run_ref(tmp_path, job)
+    assert len(rows) == 5104 // 64
+    assert all(r[2] == "ok" and r[7] == "pass" for r in rows), [r for r in rows if r[7] != "pass"][:3]
+    mine = pkg.Tuner.from_job(json.dumps(dict(job, backend={"kind": "cuda"})), str(tmp_path))
+    mine.Tune()
+    assert [r.config for r in mine.rows()] == [r[1] for r in rows]
+
+
+@pytest.mark.skipif(not BIN.exists(), reason="oracle/_ref/ref_tune_cuda not built")
+def test_reference_tuner_on_b200_host_verification(built, tmp_path):
+    job = {"template": "gemm", "problem": {"m": 256, "n": 256, "k": 256}, "device": B200,
+           "strategy": {"kind": "annealing", "fraction": "1/32768"}, "seed": 3, "verify": True}
+    rows, _ = run_ref(tmp_path, job, "host")
+    assert len(rows) == 852608 // 32768
+    assert all(r[2] == "ok" and r[7] == "pass" for r in rows), rows[:3]

@@ -139,7 +139,7 @@ def test_gemm_paper_rows_beta_and_rectangular(backend):
             (128, 128, 32, 16, 16, 1, 1, 32, 32, 0, 1, 4, 4, 2),
             (64, 64, 16, 8, 8, 1, 1, 8, 16, 1, 1, 4, 4, 8),
             (128, 128, 128, 8, 8, 1, 1, 8, 8, 1, 1, 8, 8, 8),
-            (16, 16, 16, 32, 32, 0, 1, 8, 32, 0, 1, 1, 1, 2)]
+            (32, 32, 32, 32, 32, 0, 1, 32, 32, 0, 1, 1, 1, 2)]
     names = "MWG NWG KWG MDIMC NDIMC SA SB MDIMA NDIMB STRM STRN VWM VWN KWI".split()
     for (m, n, k, a, b) in [(256, 384, 128, 1.0, 0.0), (512, 128, 256, 1.5, 0.5)]:
         want = O.gemm_reference(m, n, k, a, b)
@@ -212,3 +212,25 @@ def test_tuner_random_search_conv_verified(built):
     best, ms = t.GetBestResult()
     assert ms == min(r.time_ms for r in rows)
     assert s["kernel_launches"] > 0
+
+
+# ------------------------------------------------- TF32 tcgen05 variant
+@pytest.mark.parametrize("m,n,k", [(256, 256, 256), (512, 384, 640), (2048, 2048, 2048)])
+def test_gemm_tf32_tcgen05_configs(backend, m, n, k):
+    """Every TF32 configuration that fits the problem verifies at rel 1e-3
+    (the variant's stated tolerance) against the fp32 oracle."""
+    want = O.gemm_reference(m, n, k)
+    seen = 0
+    for bn in (64, 128, 256):
+        for bk in (32, 64):
+            for st in (2, 3, 4, 6):
+                if n % bn or k % bk or st * 4 * bk * (128 + bn) + 2048 > 232448:
+                    continue
+                cfg = dict(BN=bn, BK=bk, STAGES=st)
+                r = backend.evaluate(pkg.gemm_request(m, n, k, cfg, tf32=True))
+                assert r.ok and r.verification == "pass", (cfg, r)
+                assert r.report["max_rel_error"] < 1e-3
+                rep = O.verify(backend.read_output(m * n), want, 1e-3, 1e-6)
+                assert rep["pass"], (cfg, rep)
+                seen += 1
+    assert seen >= 6
