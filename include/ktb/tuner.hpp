@@ -8,7 +8,9 @@
 
 #include <chrono>
 #include <functional>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <string>
 #include <vector>
@@ -84,9 +86,27 @@ TuningOutcome run_tuning(const TuningJob& job, Backend& backend);
 // shared pool).  `subset`, when non-empty, replaces the unit list with those
 // enumeration indices (fixed throughput samples).  Other strategies (and a
 // single backend) fall back to run_tuning on backends[0].
+// Checkpoint of a long search: a replay table (`config,time_ms`, the format
+// of ReplayBackend) that already-evaluated successful configurations are
+// served from and new successful rows are appended to as they complete, so
+// an interrupted full search resumes where it stopped.
+class ResultLog {
+  public:
+    explicit ResultLog(const std::string& path);
+    bool lookup(const std::string& key, double* time_ms) const;
+    void append(const std::string& key, double time_ms);
+    size_t known() const { return table_.size(); }
+
+  private:
+    std::map<std::string, double> table_;
+    std::string path_;
+    std::mutex mu_;
+};
+
 TuningOutcome run_tuning_sharded(const TuningJob& job, const std::vector<Backend*>& backends,
                                  const SearchSpace& effective,
-                                 const std::vector<uint64_t>& subset = {});
+                                 const std::vector<uint64_t>& subset = {},
+                                 ResultLog* log = nullptr);
 
 // Row bookkeeping shared by both drivers: turns a backend result into a row
 // (applying the verification rule of tuner.hpp:256-289) and returns the

@@ -306,6 +306,11 @@ int ktc_tuner_set_devices(ktc_tuner* t, const int* ordinals, int n);
 /* Optional: restrict the search to these enumeration indices of the
  * composed space (used for fixed throughput samples and sharding). */
 int ktc_tuner_set_subset(ktc_tuner* t, const uint64_t* indices, size_t n);
+/* Checkpoint/resume for full and random searches: successful rows are
+ * appended to `path` (replay format `config,time_ms`) as they complete, and
+ * configurations already recorded there are served from it instead of being
+ * re-evaluated.  NULL or "" disables. */
+int ktc_tuner_set_checkpoint(ktc_tuner* t, const char* path);
 
 /* Space funnel: raw, constraint-satisfying, valid after device limits. */
 int ktc_tuner_space_counts(ktc_tuner* t, unsigned long long* raw,

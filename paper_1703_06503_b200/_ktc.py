@@ -204,6 +204,7 @@ _SIGS = {
     "ktc_tuner_set_backend": (C.c_int, [_P, C.c_char_p, C.POINTER(BackendOptions)]),
     "ktc_tuner_set_devices": (C.c_int, [_P, C.POINTER(C.c_int), C.c_int]),
     "ktc_tuner_set_subset": (C.c_int, [_P, C.POINTER(C.c_uint64), C.c_size_t]),
+    "ktc_tuner_set_checkpoint": (C.c_int, [_P, C.c_char_p]),
     "ktc_tuner_space_counts": (C.c_int, [_P, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong),
                                          C.POINTER(C.c_ulonglong)]),
     "ktc_tuner_space_config": (C.c_int, [_P, C.c_uint64, C.c_char_p, C.c_size_t]),

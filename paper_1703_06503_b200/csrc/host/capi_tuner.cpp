@@ -28,6 +28,7 @@ struct ktc_tuner {
     ktc_backend_options opts{};
     std::vector<int> devices{0};
     std::vector<uint64_t> subset;
+    std::string checkpoint;
     std::string output = "results.csv";
     std::optional<SearchSpace> effective;
     std::vector<std::unique_ptr<Backend>> backends;
@@ -513,7 +514,9 @@ void tune(ktc_tuner* t) {
     for (Backend* b : bes)
         if (auto* c = dynamic_cast<CudaBackend*>(b)) c->reset_totals();
     auto t0 = std::chrono::steady_clock::now();
-    TuningOutcome o = run_tuning_sharded(t->job, bes, eff, t->subset);
+    std::unique_ptr<ResultLog> log;
+    if (!t->checkpoint.empty()) log = std::make_unique<ResultLog>(t->checkpoint);
+    TuningOutcome o = run_tuning_sharded(t->job, bes, eff, t->subset, log.get());
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     ktc_summary& s = t->summary;
     std::memset(&s, 0, sizeof(s));
@@ -742,6 +745,11 @@ int ktc_tuner_set_devices(ktc_tuner* t, const int* ordinals, int n) {
 
 int ktc_tuner_set_subset(ktc_tuner* t, const uint64_t* indices, size_t n) {
     return guard([&] { t->subset.assign(indices, indices + n); });
+}
+
+int ktc_tuner_set_checkpoint(ktc_tuner* t, const char* path) {
+    t->checkpoint = path ? path : "";
+    return KTC_OK;
 }
 
 int ktc_tuner_space_counts(ktc_tuner* t, unsigned long long* raw, unsigned long long* constrained,

@@ -5,6 +5,7 @@
 #include <atomic>
 #include <charconv>
 #include <cmath>
+#include <fstream>
 #include <mutex>
 #include <ostream>
 #include <thread>
@@ -236,8 +237,29 @@ TuningOutcome run_tuning(const TuningJob& job, Backend& backend) {
 // earliest wins, search.hpp:203-208).
 // ---------------------------------------------------------------------------
 
+ResultLog::ResultLog(const std::string& path) : path_(path) {
+    std::ifstream probe(path, std::ios::binary);
+    if (probe) table_ = ReplayBackend::load(path).table();
+    else ReplayBackend::save(path, {});  // header only
+}
+
+bool ResultLog::lookup(const std::string& key, double* t) const {
+    auto it = table_.find(key);
+    if (it == table_.end()) return false;
+    *t = it->second;
+    return true;
+}
+
+void ResultLog::append(const std::string& key, double t) {
+    std::lock_guard<std::mutex> lk(mu_);
+    if (!table_.emplace(key, t).second) return;
+    std::ofstream out(path_, std::ios::binary | std::ios::app);
+    out << key << ',' << format_double(t) << '\n';
+}
+
 TuningOutcome run_tuning_sharded(const TuningJob& job, const std::vector<Backend*>& backends,
-                                 const SearchSpace& eff, const std::vector<uint64_t>& subset) {
+                                 const SearchSpace& eff, const std::vector<uint64_t>& subset,
+                                 ResultLog* log) {
     if (backends.empty()) throw Error("run_tuning_sharded: no backends");
     const bool ordered = job.strategy.kind == StrategyKind::full ||
                          job.strategy.kind == StrategyKind::random;
@@ -289,8 +311,19 @@ TuningOutcome run_tuning_sharded(const TuningJob& job, const std::vector<Backend
                     row.space_index = units[i];
                     row.device = be.device();
                     EvaluationRequest req = make_request(job, row.config, &row.sizes);
+                    double known = 0.0;
+                    if (log && log->lookup(row.config.canonical(), &known)) {
+                        // Checkpointed: only verified successes are logged.
+                        row.status = Status::success;
+                        row.time_ms = known;
+                        row.verification = job.verify ? Verification::pass : Verification::skipped;
+                        row.message = "resumed from checkpoint";
+                        times[i] = known;
+                        continue;
+                    }
                     EvaluationResult res = be.evaluate(req);
                     times[i] = finish_row(job, res, row, &reference, &digests);
+                    if (log && times[i]) log->append(row.config.canonical(), *times[i]);
                 }
             }
         } catch (const std::exception& e) {

@@ -85,6 +85,10 @@ __device__ __forceinline__ void vstore(float* p, const float* s) {
 #define VB (NWG / VWN)
 #define NVB ((VB >= NDIMB) ? (VB / NDIMB) : 1)
 #endif
+// Register double buffering of the shared-memory copies when their staging
+// registers (per thread) stay small.
+#define STAGE_REGS ((SA ? KWA * MVA * VWM : 0) + (SB ? KWB * NVB * VWN : 0))
+#define STAGE_AHEAD (STAGE_REGS <= 32)
 
 extern "C" __global__ void __launch_bounds__(NT, 1)
 KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float beta,
@@ -112,46 +116,83 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
 #pragma unroll
         for (int j = 0; j < NWI; ++j) acc[i][j] = 0.0f;
 
-#pragma unroll 1
-    for (int k0 = 0; k0 < K; k0 += KWG) {
+    // Shared-memory tiles are copied through registers by the MDIMA x KDIMA
+    // (MDIMB x KDIMB) thread re-shape.  When the staging registers are few,
+    // the NEXT K-tile's global loads are issued before computing on the
+    // current one (register double buffering), hiding their latency.
 #if SA
-        {
-            const int la0 = tid % MDIMA, la1 = tid / MDIMA;
-            if (VA >= MDIMA || la0 < VA) {
+    const int la0 = tid % MDIMA, la1 = tid / MDIMA;
+    const bool a_copies = (VA >= MDIMA) || (la0 < VA);
+    float ra[KWA][MVA * VWM];
+#endif
+#if SB
+    const int lb0 = tid % NDIMB, lb1 = tid / NDIMB;
+    const bool b_copies = (VB >= NDIMB) || (lb0 < VB);
+    float rb[KWB][NVB * VWN];
+#endif
+    auto fetch = [&](int kk0) {
+#if SA
+        if (a_copies) {
 #pragma unroll
-                for (int kia = 0; kia < KWA; ++kia) {
-                    const int k = la1 * KWA + kia;
+            for (int kia = 0; kia < KWA; ++kia)
 #pragma unroll
-                    for (int mia = 0; mia < MVA; ++mia) {
-                        const int mv = STRM ? (la0 + mia * MDIMA) : (mia + la0 * MVA);
-                        float v[VWM];
-                        vload_g<VWM>(v, A + (size_t)(k0 + k) * M + m0 + mv * VWM);
-                        vstore<VWM>(alm + k * MWG + mv * VWM, v);
-                    }
+                for (int mia = 0; mia < MVA; ++mia) {
+                    const int mv = STRM ? (la0 + mia * MDIMA) : (mia + la0 * MVA);
+                    vload_g<VWM>(&ra[kia][mia * VWM],
+                                 A + (size_t)(kk0 + la1 * KWA + kia) * M + m0 + mv * VWM);
                 }
-            }
         }
 #endif
 #if SB
-        {
-            const int lb0 = tid % NDIMB, lb1 = tid / NDIMB;
-            if (VB >= NDIMB || lb0 < VB) {
+        if (b_copies) {
 #pragma unroll
-                for (int kib = 0; kib < KWB; ++kib) {
-                    const int k = lb1 * KWB + kib;
+            for (int kib = 0; kib < KWB; ++kib)
 #pragma unroll
-                    for (int nib = 0; nib < NVB; ++nib) {
-                        const int nv = STRN ? (lb0 + nib * NDIMB) : (nib + lb0 * NVB);
-                        float v[VWN];
-                        vload_g<VWN>(v, B + (size_t)(k0 + k) * N + n0 + nv * VWN);
-                        vstore<VWN>(blm + k * NWG + nv * VWN, v);
-                    }
+                for (int nib = 0; nib < NVB; ++nib) {
+                    const int nv = STRN ? (lb0 + nib * NDIMB) : (nib + lb0 * NVB);
+                    vload_g<VWN>(&rb[kib][nib * VWN],
+                                 B + (size_t)(kk0 + lb1 * KWB + kib) * N + n0 + nv * VWN);
                 }
-            }
         }
 #endif
+        (void)kk0;
+    };
+    auto stash = [&]() {
+#if SA
+        if (a_copies) {
+#pragma unroll
+            for (int kia = 0; kia < KWA; ++kia)
+#pragma unroll
+                for (int mia = 0; mia < MVA; ++mia) {
+                    const int mv = STRM ? (la0 + mia * MDIMA) : (mia + la0 * MVA);
+                    vstore<VWM>(alm + (la1 * KWA + kia) * MWG + mv * VWM, &ra[kia][mia * VWM]);
+                }
+        }
+#endif
+#if SB
+        if (b_copies) {
+#pragma unroll
+            for (int kib = 0; kib < KWB; ++kib)
+#pragma unroll
+                for (int nib = 0; nib < NVB; ++nib) {
+                    const int nv = STRN ? (lb0 + nib * NDIMB) : (nib + lb0 * NVB);
+                    vstore<VWN>(blm + (lb1 * KWB + kib) * NWG + nv * VWN, &rb[kib][nib * VWN]);
+                }
+        }
+#endif
+    };
 #if SA || SB
+    fetch(0);
+#endif
+
+#pragma unroll 1
+    for (int k0 = 0; k0 < K; k0 += KWG) {
+#if SA || SB
+        stash();
         __syncthreads();
+#if STAGE_AHEAD
+        if (k0 + KWG < K) fetch(k0 + KWG);
+#endif
 #endif
 
 #pragma unroll 1
@@ -186,6 +227,9 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
         }
 #if SA || SB
         __syncthreads();
+#if !STAGE_AHEAD
+        if (k0 + KWG < K) fetch(k0 + KWG);
+#endif
 #endif
     }
 
@@ -228,3 +272,5 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
 #undef KWB
 #undef VB
 #undef NVB
+#undef STAGE_REGS
+#undef STAGE_AHEAD

@@ -183,6 +183,10 @@ class Tuner:
         arr, n = _arr(C.c_uint64, indices)
         K.check(self._lib.ktc_tuner_set_subset(self._h, arr, n))
 
+    def SetCheckpoint(self, path: str | None):
+        """Resume file for long full/random searches (replay CSV format)."""
+        K.check(self._lib.ktc_tuner_set_checkpoint(self._h, (path or "").encode()))
+
     # ---------------------------------------------------------------- space
     def space_counts(self) -> tuple[int, int, int]:
         raw, con, val = C.c_ulonglong(), C.c_ulonglong(), C.c_ulonglong()
