@@ -345,24 +345,36 @@ def main():
 def tuned_block(pkg, local, threads, sample_best, peaks) -> dict:
     """Re-times the per-filter winners (configs[1]) and the SGEMM winner."""
     table = tuned_table()
+    # `be`: the tuner's protocol (L2 flushed, best of 10).  `sus`: 30
+    # back-to-back launches without flushes, mean launch time -- the
+    # sustained figure the roofline uses (each launch also pays for the
+    # previous launch's L2 write-backs, as in a real pipeline).
     be = pkg.CudaBackend(local, compile_threads=threads)
+    sus = pkg.CudaBackend(local, compile_threads=threads, flush_l2=False, warmup=3)
     fp32_peak = fp32_peak_gflops()
-    out = {"conv": {}, "source": "tuned/b200_winners.json" if table else "this run's sample"}
+    out = {"conv": {}, "source": "tuned/b200_winners.json" if table else "this run's sample",
+           "timing": "time_ms: best of 10 flushed launches; mean_ms: mean of 30 back-to-back "
+                     "launches (roofline uses mean_ms)"}
     for f in (3, 5, 7, 9, 11):
         entry = table.get("conv", {}).get(str(f))
         cfg = entry["config"] if entry else (sample_best.config if f == 3 else None)
         if not cfg:
             continue
-        r = be.evaluate(pkg.conv_request(X, Y, f, pkg.parse_canonical(cfg), reps=10))
-        if not r.ok:
+        req = pkg.conv_request(X, Y, f, pkg.parse_canonical(cfg), reps=10)
+        r = be.evaluate(req)
+        req.repetitions = 30
+        rs = sus.evaluate(req)
+        if not (r.ok and rs.ok):
             out["conv"][str(f)] = {"config": cfg, "status": r.status, "message": r.message}
             continue
-        gflops = conv_flops(f) / (r.time_ms * 1e-3) / 1e9
-        gbs = CONV_BYTES / (r.time_ms * 1e-3) / 1e9
+        mean = rs.mean_ms
+        gflops = conv_flops(f) / (mean * 1e-3) / 1e9
+        gbs = CONV_BYTES / (mean * 1e-3) / 1e9
         ai = conv_flops(f) / CONV_BYTES
         bound = "hbm" if ai < fp32_peak / peaks["hbm_gbs"] else "fp32"
         out["conv"][str(f)] = {
-            "config": cfg, "time_ms": r.time_ms, "gflops": gflops, "gbs": gbs,
+            "config": cfg, "time_ms": r.time_ms, "mean_ms": mean, "gflops": gflops, "gbs": gbs,
+            "gflops_best": conv_flops(f) / (r.time_ms * 1e-3) / 1e9,
             "verified": r.verification, "bound": bound,
             "frac_hbm": gbs / peaks["hbm_gbs"], "frac_fp32": gflops / fp32_peak,
             "frac": gbs / peaks["hbm_gbs"] if bound == "hbm" else gflops / fp32_peak,
@@ -371,10 +383,15 @@ def tuned_block(pkg, local, threads, sample_best, peaks) -> dict:
     g = table.get("gemm", {}).get("2048")
     if g:
         m = 2048
-        r = be.evaluate(pkg.gemm_request(m, m, m, pkg.parse_canonical(g["config"]), reps=10))
-        if r.ok:
-            gf = 2.0 * m ** 3 / (r.time_ms * 1e-3) / 1e9
-            out["sgemm_2048"] = {"config": g["config"], "time_ms": r.time_ms, "gflops": gf,
+        req = pkg.gemm_request(m, m, m, pkg.parse_canonical(g["config"]), reps=10)
+        r = be.evaluate(req)
+        req.repetitions = 30
+        rs = sus.evaluate(req)
+        if r.ok and rs.ok:
+            gf = 2.0 * m ** 3 / (rs.mean_ms * 1e-3) / 1e9
+            out["sgemm_2048"] = {"config": g["config"], "time_ms": r.time_ms,
+                                 "mean_ms": rs.mean_ms, "gflops": gf,
+                                 "gflops_best": 2.0 * m ** 3 / (r.time_ms * 1e-3) / 1e9,
                                  "verified": r.verification, "bound": "fp32",
                                  "frac": gf / fp32_peak}
     t = table.get("gemm_tf32", {}).get("2048")
@@ -388,6 +405,7 @@ def tuned_block(pkg, local, threads, sample_best, peaks) -> dict:
                                 "verified": r.verification, "tolerance": "rel 1e-3, abs 1e-6"}
     out["fp32_peak_gflops"] = fp32_peak
     be.close()
+    sus.close()
     return out
 
 

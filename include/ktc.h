@@ -216,6 +216,7 @@ typedef struct {
     double verify_ms;     /* device verification */
     int compile_cache_hit;
     int kernel_launches;  /* kernels of this library launched for this evaluation */
+    double mean_ms;       /* mean over the timed repetitions (time_ms is the min) */
 } ktc_result;
 
 typedef struct {

@@ -88,7 +88,7 @@ class Result(C.Structure):
         ("output_digests", (C.c_char * 17) * MAX_OUTPUTS), ("verification", C.c_int),
         ("report", VerifyReport), ("message", C.c_char * 512), ("compile_ms", C.c_double),
         ("load_ms", C.c_double), ("run_ms", C.c_double), ("verify_ms", C.c_double),
-        ("compile_cache_hit", C.c_int), ("kernel_launches", C.c_int),
+        ("compile_cache_hit", C.c_int), ("kernel_launches", C.c_int), ("mean_ms", C.c_double),
     ]
 
 

@@ -44,6 +44,7 @@ class Result:
     verify_ms: float = 0.0
     cache_hit: bool = False
     launches: int = 0
+    mean_ms: float = 0.0
 
     @property
     def ok(self) -> bool:
@@ -165,7 +166,7 @@ class CudaBackend:
                      if out.output_digests[i].value],
             compile_ms=out.compile_ms, load_ms=out.load_ms, run_ms=out.run_ms,
             verify_ms=out.verify_ms, cache_hit=bool(out.compile_cache_hit),
-            launches=out.kernel_launches)
+            launches=out.kernel_launches, mean_ms=out.mean_ms)
 
     def prefetch(self, req: Request) -> None:
         r, _keep = self._build(req)

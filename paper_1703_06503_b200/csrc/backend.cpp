@@ -561,6 +561,8 @@ bool plan_gemm_tf32(ktc_backend* be, const ktc_request* r, Plan* p, std::string*
     }
     p->ksrc = &tf32_source();
     p->config = {define("BN", BN), define("BK", BK), define("STAGES", STAGES)};
+    if (const char* v = std::getenv("KTC_TF32_DESC_VARIANT"))  // layout experiments
+        p->config.push_back(define("DESC_VARIANT", std::atoi(v)));
     p->smem = unsigned(STAGES * 4 * BK * (128 + BN) + 2048);
     if (p->smem > be->ctx->limits.smem_per_block_optin) {
         *why = "needs " + std::to_string(p->smem) + " bytes of shared memory";
@@ -703,8 +705,11 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
                 cuuint32_t estr[2] = {1, 1};
                 return d.cuTensorMapEncodeTiled(
                     m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, reinterpret_cast<void*>(base), dims,
-                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    // MN-major TF32 operands need UMMA's SW128_32B layout:
+                    // 128-byte rows, 32-byte swizzle atoms (4-row groups).
+                    CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             };
             CUresult rc = encode(&tmap, I.dev[5], I.M, I.K);
             if (rc == CUDA_SUCCESS) rc = encode(&tmap2, I.dev[6], I.N, I.K);
@@ -773,8 +778,12 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
     const long long launches0 = ctx->launches;
     float best = 0.0f;
     const int reps = r->repetitions > 0 ? r->repetitions : 1;
+    std::vector<float> all(size_t(reps), 0.0f);
     st = ktc_launch_timed(ctx, fn, plan.grid, plan.block, plan.smem, params.data(),
-                          be->opts.warmup, reps, be->opts.flush_l2, &best, nullptr);
+                          be->opts.warmup, reps, be->opts.flush_l2, &best, all.data());
+    double sum = 0.0;
+    for (float v : all) sum += v;
+    out->mean_ms = sum / double(reps);
     out->run_ms = ms_since(t0);
     if (st) {
         set_msg(out, last_error());

@@ -151,55 +151,76 @@ __device__ __forceinline__ void vp_block_reduce(VerifyPartial& p, VerifyPartial*
     }
 }
 
-template <bool IS_F32>
-__device__ __forceinline__ void vp_element(VerifyPartial& p, unsigned long long i, double c,
-                                           double r, double rel_tol, double abs_tol, bool equal) {
+// One f32 element, the reference rule in double (tuner.hpp:86-93).  The
+// relative error's division is exact but rare: it is only evaluated when it
+// could raise the running maximum (abs >= max_rel * mag, with a 2^-40 margin
+// for the rounding of the product), or for the NaN / infinite corner cases.
+__device__ __forceinline__ void vp_f32(VerifyPartial& p, unsigned long long i, float cf, float rf,
+                                       double rel_tol, double abs_tol) {
+    const double c = (double)cf, r = (double)rf;
     const double abs_err = fabs(c - r);
-    double rel_err;
-    bool ok;
-    if (IS_F32) {
-        const double mag = fabs(r);
-        rel_err = mag > 0.0 ? abs_err / mag : 0.0;
-        ok = abs_err <= abs_tol + rel_tol * mag;  // false for NaN
-    } else {
-        rel_err = abs_err;
-        ok = equal;
-    }
-    if (!ok && i < p.first_fail) p.first_fail = i;
-    if (abs_err != abs_err) {
+    const double mag = fabs(r);
+    if (!(abs_err <= abs_tol + rel_tol * mag) && i < p.first_fail) p.first_fail = i;  // NaN fails
+    if (abs_err > p.max_abs) {
+        p.max_abs = abs_err;
+        p.argmax = i;
+    } else if (abs_err != abs_err) {
         p.nan_abs = (long long)i;  // indices grow per thread: last wins
-    } else if (abs_err > p.max_abs) {
+    }
+    if (mag > 0.0) {
+        if (abs_err >= p.max_rel * mag * (1.0 - 0x1.0p-40) || abs_err != abs_err ||
+            mag == __longlong_as_double(0x7ff0000000000000ll)) {
+            const double rel = abs_err / mag;
+            if (rel > p.max_rel) p.max_rel = rel;
+            else if (rel != rel) p.nan_rel = (long long)i;
+        }
+    } else if (0.0 > p.max_rel) {
+        p.max_rel = 0.0;  // mag == 0 (or NaN): the reference's rel_err is 0
+    }
+}
+
+__device__ __forceinline__ void vp_i32(VerifyPartial& p, unsigned long long i, int ci, int ri) {
+    const double abs_err = fabs((double)ci - (double)ri);
+    if (ci != ri && i < p.first_fail) p.first_fail = i;
+    if (abs_err > p.max_abs) {
         p.max_abs = abs_err;
         p.argmax = i;
     }
-    if (rel_err != rel_err) p.nan_rel = (long long)i;
-    else if (rel_err > p.max_rel) p.max_rel = rel_err;
+    if (abs_err > p.max_rel) p.max_rel = abs_err;
 }
 
-// Each block owns one contiguous chunk; threads stride within it, so a
-// thread's indices are increasing (needed for the nan_* "last" updates).
+// Each block owns one contiguous chunk (a multiple of 4 elements); threads
+// stride through it in float4 steps, so a thread's indices are increasing
+// (needed for the nan_* "last" updates).
 extern "C" __global__ void __launch_bounds__(KTC_VERIFY_THREADS)
 ktc_verify_partial(const void* __restrict__ cand, const void* __restrict__ ref,
                    unsigned long long n, int is_f32, double rel_tol, double abs_tol,
                    VerifyPartial* __restrict__ partials) {
     VerifyPartial p;
     vp_init(p);
-    const unsigned long long chunk = (n + gridDim.x - 1) / gridDim.x;
+    const unsigned long long chunk = ((n + gridDim.x - 1) / gridDim.x + 3) & ~3ull;
     const unsigned long long begin = chunk * blockIdx.x;
     const unsigned long long end = begin + chunk < n ? begin + chunk : n;
     if (is_f32) {
         const float* c = (const float*)cand;
         const float* r = (const float*)ref;
-        for (unsigned long long i = begin + threadIdx.x; i < end; i += KTC_VERIFY_THREADS)
-            vp_element<true>(p, i, (double)__ldg(c + i), (double)__ldg(r + i), rel_tol, abs_tol,
-                             false);
+        const unsigned long long end4 = begin + ((end > begin ? end - begin : 0) & ~3ull);
+        for (unsigned long long i = begin + 4ull * threadIdx.x; i < end4;
+             i += 4ull * KTC_VERIFY_THREADS) {
+            const float4 cv = __ldg(reinterpret_cast<const float4*>(c + i));
+            const float4 rv = __ldg(reinterpret_cast<const float4*>(r + i));
+            vp_f32(p, i, cv.x, rv.x, rel_tol, abs_tol);
+            vp_f32(p, i + 1, cv.y, rv.y, rel_tol, abs_tol);
+            vp_f32(p, i + 2, cv.z, rv.z, rel_tol, abs_tol);
+            vp_f32(p, i + 3, cv.w, rv.w, rel_tol, abs_tol);
+        }
+        for (unsigned long long i = end4 + threadIdx.x; i < end; i += KTC_VERIFY_THREADS)
+            vp_f32(p, i, __ldg(c + i), __ldg(r + i), rel_tol, abs_tol);
     } else {
         const int* c = (const int*)cand;
         const int* r = (const int*)ref;
-        for (unsigned long long i = begin + threadIdx.x; i < end; i += KTC_VERIFY_THREADS) {
-            const int ci = __ldg(c + i), ri = __ldg(r + i);
-            vp_element<false>(p, i, (double)ci, (double)ri, 0.0, 0.0, ci == ri);
-        }
+        for (unsigned long long i = begin + threadIdx.x; i < end; i += KTC_VERIFY_THREADS)
+            vp_i32(p, i, __ldg(c + i), __ldg(r + i));
     }
     vp_block_reduce(p, partials + blockIdx.x);
 }

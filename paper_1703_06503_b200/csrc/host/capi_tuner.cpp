@@ -814,7 +814,8 @@ int ktc_tuner_write_replay(ktc_tuner* t, const char* path) {
         if (!t->outcome) throw Error("Tune() has not run");
         std::map<std::string, double> table;
         for (const TuningRow& r : t->outcome->rows)
-            if (r.status == Status::success && r.time_ms) table.emplace(r.config.canonical(), *r.time_ms);
+            if (r.status == Status::success && r.time_ms && r.verification != Verification::fail)
+                table.emplace(r.config.canonical(), *r.time_ms);
         ReplayBackend::save(path, table);
     });
 }

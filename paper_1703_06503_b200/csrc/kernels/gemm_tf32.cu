@@ -68,17 +68,20 @@ __device__ __forceinline__ void tma_load_2d(u32 dst, const TensorMap* map, u32 b
         : "memory");
 }
 
-// UMMA shared-memory descriptor, MN-major SWIZZLE_128B (sm_100 layout):
-// start>>4 [0,14), LBO>>4 [16,30) = stride between 32-element MN atoms,
-// SBO>>4 [32,46) = stride between 8-row K groups, version 1 at [46,48),
-// layout type 2 (SWIZZLE_128B) at [61,64).
+// UMMA shared-memory descriptor for MN-major 32-bit operands (sm_100): the
+// only layout UMMA accepts for MN-major TF32 is SWIZZLE_128B_BASE32B
+// (128-byte MN rows, 32-byte swizzle atoms over 4-row K groups), which is
+// what TMA's SWIZZLE_128B_ATOM_32B mode writes.  Fields: start>>4 [0,14),
+// LBO>>4 [16,30) = stride between 32-element MN atoms, SBO>>4 [32,46) =
+// stride between 4-row K groups, version 1 at [46,48), layout type 1 at
+// [61,64).
 __device__ __forceinline__ u64 umma_desc(u32 addr, u32 lbo, u32 sbo) {
     u64 d = 0;
     d |= (u64)((addr >> 4) & 0x3FFF);
     d |= (u64)((lbo >> 4) & 0x3FFF) << 16;
     d |= (u64)((sbo >> 4) & 0x3FFF) << 32;
     d |= (u64)1 << 46;
-    d |= (u64)2 << 61;
+    d |= (u64)1 << 61;
     return d;
 }
 
@@ -200,8 +203,17 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
             const u32 sb = sa + A_STAGE_BYTES;
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
-                const u64 ad = umma_desc(sa + kk * 1024, A_BOX_BYTES, 1024);
-                const u64 bd = umma_desc(sb + kk * 1024, A_BOX_BYTES, 1024);
+                // K = 8 per MMA = two 4-row groups of 512 B.
+#ifndef DESC_VARIANT
+#define DESC_VARIANT 0
+#endif
+#if DESC_VARIANT == 0
+                const u64 ad = umma_desc(sa + kk * 1024, A_BOX_BYTES, 512);
+                const u64 bd = umma_desc(sb + kk * 1024, A_BOX_BYTES, 512);
+#else
+                const u64 ad = umma_desc(sa + kk * 1024, 512, A_BOX_BYTES);
+                const u64 bd = umma_desc(sb + kk * 1024, 512, A_BOX_BYTES);
+#endif
                 umma_tf32(tmem, ad, bd, make_idesc(BN), (kb | kk) != 0 ? 1u : 0u);
             }
             umma_commit(empty0 + 8 * s);  // stage reusable once these MMAs retire
