@@ -205,15 +205,26 @@ ktc_verify_partial(const void* __restrict__ cand, const void* __restrict__ ref,
         const float* c = (const float*)cand;
         const float* r = (const float*)ref;
         const unsigned long long end4 = begin + ((end > begin ? end - begin : 0) & ~3ull);
+        // Four independent partial states (one per float4 lane) break the
+        // running-max dependency chain; each lane's indices still increase,
+        // and vp_merge is the same exact rule used across threads.
+        VerifyPartial q1, q2, q3;
+        vp_init(q1);
+        vp_init(q2);
+        vp_init(q3);
+#pragma unroll 2
         for (unsigned long long i = begin + 4ull * threadIdx.x; i < end4;
              i += 4ull * KTC_VERIFY_THREADS) {
             const float4 cv = __ldg(reinterpret_cast<const float4*>(c + i));
             const float4 rv = __ldg(reinterpret_cast<const float4*>(r + i));
             vp_f32(p, i, cv.x, rv.x, rel_tol, abs_tol);
-            vp_f32(p, i + 1, cv.y, rv.y, rel_tol, abs_tol);
-            vp_f32(p, i + 2, cv.z, rv.z, rel_tol, abs_tol);
-            vp_f32(p, i + 3, cv.w, rv.w, rel_tol, abs_tol);
+            vp_f32(q1, i + 1, cv.y, rv.y, rel_tol, abs_tol);
+            vp_f32(q2, i + 2, cv.z, rv.z, rel_tol, abs_tol);
+            vp_f32(q3, i + 3, cv.w, rv.w, rel_tol, abs_tol);
         }
+        vp_merge(p, q1);
+        vp_merge(p, q2);
+        vp_merge(p, q3);
         for (unsigned long long i = end4 + threadIdx.x; i < end; i += KTC_VERIFY_THREADS)
             vp_f32(p, i, __ldg(c + i), __ldg(r + i), rel_tol, abs_tol);
     } else {
