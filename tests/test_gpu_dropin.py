@@ -50,3 +50,24 @@ def test_reference_tuner_on_b200_host_verification(built, tmp_path):
     rows, _ = run_ref(tmp_path, job, "host")
     assert len(rows) == 852608 // 32768
     assert all(r[2] == "ok" and r[7] == "pass" for r in rows), rows[:3]
+
+
+RUNNER = Path(pkg.__file__).resolve().parent / "ktune-cuda-runner"
+
+
+@pytest.mark.skipif(not O.ref_available() or not RUNNER.exists(), reason="runner / oracle not built")
+def test_reference_external_backend_drives_b200_runner(built, tmp_path):
+    """Zero-change integration: the reference's own ExternalBackend
+    (external.hpp) spawns ktune-cuda-runner per evaluation; every row comes
+    back ok and verified through the protocol's output digests."""
+    job = {"template": "conv", "problem": {"x": 512, "y": 256, "filter": 5}, "device": B200,
+           "strategy": {"kind": "random", "fraction": "1/512"}, "seed": 3, "verify": True,
+           "backend": {"kind": "external", "argv": [str(RUNNER)], "timeout_ms": 120000}}
+    import os
+
+    os.environ["KTC_CACHE_DIR"] = str(tmp_path / "cubins")
+    bi, bt = O.ref_job_run(json.dumps(job), str(tmp_path), str(tmp_path / "ref.csv"))
+    rows = [ln.split(",") for ln in (tmp_path / "ref.csv").read_bytes().decode().split("\r\n")[1:-1]]
+    assert len(rows) == 5104 // 512
+    assert all(r[2] == "ok" and r[7] == "pass" for r in rows), rows
+    assert bi >= 0 and bt > 0
