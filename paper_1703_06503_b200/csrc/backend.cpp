@@ -211,6 +211,44 @@ bool check_layout(const ktc_request* r, Family fam, std::string* why) {
     return false;
 }
 
+// Host copies of materialized recipes, in pinned memory, shared by every
+// backend of the process: a job's inputs are a pure function of their recipe
+// (arguments.hpp:126-180), so a new job over the same problem only pays the
+// H2D copy.  Bounded (LRU by insertion) to 4 GiB.
+struct PinnedInput {
+    void* host = nullptr;
+    size_t bytes = 0;
+    ~PinnedInput() {
+        if (host) driver().cuMemFreeHost(host);
+    }
+};
+
+std::shared_ptr<PinnedInput> pinned_recipe(const ktb::ArgumentSpec& a) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::string, std::shared_ptr<PinnedInput>>> cache;
+    const std::string key = std::string(ktb::to_string(a.type)) + "|" + a.fill + "|" +
+                            std::to_string(a.length);
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& e : cache)
+        if (e.first == key) return e.second;
+    auto p = std::make_shared<PinnedInput>();
+    p->bytes = a.length * 4;
+    if (driver().cuMemHostAlloc(&p->host, p->bytes ? p->bytes : 4, CU_MEMHOSTALLOC_PORTABLE) !=
+        CUDA_SUCCESS) {
+        p->host = nullptr;
+        throw ktb::Error("cuMemHostAlloc failed for a " + std::to_string(p->bytes) + "-byte input");
+    }
+    ktb::materialize_into(a, p->host);
+    size_t total = p->bytes;
+    for (auto& e : cache) total += e.second->bytes;
+    while (!cache.empty() && total > (size_t(4) << 30)) {
+        total -= cache.front().second->bytes;
+        cache.erase(cache.begin());
+    }
+    cache.emplace_back(key, p);
+    return p;
+}
+
 // Materializes, uploads and (for the built-in families) computes the device
 // reference.  Throws nothing; returns a ktc.h code.
 int build_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
@@ -249,15 +287,14 @@ int build_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
         // and every row start is 16-byte aligned for float4 / TMA.
         I.ipitch = int(round_up(round_up(size_t(I.X), 512) + I.F + 8, 64));
         I.rows = int(round_up(size_t(I.Y), 512) + I.F + 32);
-        std::vector<float> img(px * py);
-        ktb::materialize_into(I.args[4], img.data());
+        std::shared_ptr<PinnedInput> img = pinned_recipe(I.args[4]);
         I.taps.resize(size_t(I.F) * I.F);
         ktb::materialize_into(I.args[5], I.taps.data());
         I.bytes[4] = size_t(I.ipitch) * I.rows * 4;
         CK(alloc(I.bytes[4], &I.dev[4]), "cuMemAlloc(image)");
         CK(d.cuMemsetD32Async(I.dev[4], 0, I.bytes[4] / 4, ctx->stream), "cuMemset(image)");
         CK(d.cuStreamSynchronize(ctx->stream), "cuStreamSynchronize");
-        int st = ktc_upload_pitched(ctx, I.dev[4], size_t(I.ipitch) * 4, img.data(), px * 4, px * 4,
+        int st = ktc_upload_pitched(ctx, I.dev[4], size_t(I.ipitch) * 4, img->host, px * 4, px * 4,
                                     py);
         if (st) return st;
         I.bytes[5] = I.taps.size() * 4;
@@ -280,11 +317,10 @@ int build_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
             return KTC_ERR_INVALID;
         }
         for (int a = 5; a <= 7; ++a) {  // A, B, C (C pristine: kernels write a separate output)
-            std::vector<float> h(I.args[a].length);
-            ktb::materialize_into(I.args[a], h.data());
-            I.bytes[a] = h.size() * 4;
+            std::shared_ptr<PinnedInput> h = pinned_recipe(I.args[a]);
+            I.bytes[a] = h->bytes;
             CK(alloc(I.bytes[a], &I.dev[a]), "cuMemAlloc(matrix)");
-            CK(d.cuMemcpyHtoD(I.dev[a], h.data(), I.bytes[a]), "cuMemcpyHtoD(matrix)");
+            CK(d.cuMemcpyHtoD(I.dev[a], h->host, I.bytes[a]), "cuMemcpyHtoD(matrix)");
         }
         I.out_arg = {7};
     } else {
@@ -342,8 +378,14 @@ int ensure_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
     std::string sig = signature(r);
     if (be->in && be->in->sig == sig) return KTC_OK;
     free_inputs(be);
-    int st = build_inputs(be, r, fam);
-    if (st) free_inputs(be);
+    int st;
+    try {
+        st = build_inputs(be, r, fam);
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        st = KTC_ERR_INVALID;
+    }
+    if (st) free_inputs(be);  // never leave a half-built argument list cached
     return st;
 }
 
@@ -436,6 +478,28 @@ bool plan_conv(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
     return true;
 }
 
+// Upper bound on the double-buffered GEMM tile footprint (bytes).  112 KiB
+// keeps two CTAs per SM; KTC_GEMM_DBUF_MAX overrides it (0 disables) for
+// A/B experiments.
+size_t gemm_dbuf_max_bytes() {
+    static const size_t v = [] {
+        const char* e = std::getenv("KTC_GEMM_DBUF_MAX");
+        return e ? size_t(std::strtoull(e, nullptr, 10)) : size_t(112 * 1024);
+    }();
+    return v;
+}
+
+// Register-budget policy handed to the kernel (gemm.cu OCC): 1 = estimate
+// the live registers and ask ptxas for the matching CTAs per SM; 0 = leave
+// ptxas the full 255-register budget.  KTC_GEMM_OCC overrides.
+int gemm_occ_policy() {
+    static const int v = [] {
+        const char* e = std::getenv("KTC_GEMM_OCC");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why) {
     const Inputs& I = *be->in;
     ParamView pv{r};
@@ -478,7 +542,15 @@ bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
                define("SB", SB ? 1 : 0), define("MDIMA", MDIMA), define("NDIMB", NDIMB),
                define("STRM", v[9] ? 1 : 0), define("STRN", v[10] ? 1 : 0), define("VWM", VWM),
                define("VWN", VWN), define("KWI", KWI)};
-    p->smem = unsigned((SA * KWG * MWG + SB * KWG * NWG) * 4);
+    // Double-buffered cp.async tiles when two copies of the staged tiles
+    // stay within gemm_dbuf_max_bytes() (so a second CTA still fits per SM);
+    // otherwise the single-buffer, register-staged copy.
+    const unsigned tile_bytes = unsigned((SA * KWG * MWG + SB * KWG * NWG) * 4);
+    const bool dbuf = (SA || SB) && 2 * size_t(tile_bytes) <= gemm_dbuf_max_bytes() &&
+                      2 * size_t(tile_bytes) <= be->ctx->limits.smem_per_block_optin;
+    p->config.push_back(define("DBUF", dbuf ? 1 : 0));
+    p->config.push_back(define("OCC", gemm_occ_policy()));
+    p->smem = dbuf ? 2 * tile_bytes : tile_bytes;
     if (p->smem > be->ctx->limits.smem_per_block_optin) {
         *why = "needs " + std::to_string(p->smem) + " bytes of shared memory";
         return false;

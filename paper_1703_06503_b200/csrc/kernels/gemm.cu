@@ -66,7 +66,30 @@ __device__ __forceinline__ void vstore(float* p, const float* s) {
     }
 }
 
+// Asynchronous global -> shared copy of N floats (cp.async; 16-byte pieces
+// bypass L1).  Used for double-buffered tiles: no staging registers.
+template <int N>
+__device__ __forceinline__ void cp_async(float* s, const float* __restrict__ g) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(s));
+    if (N == 1) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(g) : "memory");
+    } else if (N == 2) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g) : "memory");
+    } else {
+#pragma unroll
+        for (int q = 0; q < N; q += 4)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 4 * q), "l"(g + q)
+                         : "memory");
+    }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 //@@KTC_BODY@@ -- instantiated once per configuration; KTC_ENTRY names the kernel.
+#ifndef DBUF  // host-chosen (backend.cpp plan_gemm): double-buffered cp.async tiles
+#define DBUF 0
+#define KTC_DBUF_DEFAULT
+#endif
 #define MWI (MWG / MDIMC)
 #define NWI (NWG / NDIMC)
 #define NT (MDIMC * NDIMC)
@@ -78,19 +101,37 @@ __device__ __forceinline__ void vstore(float* p, const float* s) {
 #define KWA (KWG / KDIMA)
 #define VA (MWG / VWM)                          // A vectors per k-row of the tile
 #define MVA ((VA >= MDIMA) ? (VA / MDIMA) : 1)  // per copying thread
+#define STAGE_A (KWA * MVA * VWM)
+#else
+#define STAGE_A 0
 #endif
 #if SB
 #define KDIMB (NT / NDIMB)
 #define KWB (KWG / KDIMB)
 #define VB (NWG / VWN)
 #define NVB ((VB >= NDIMB) ? (VB / NDIMB) : 1)
+#define STAGE_B (KWB * NVB * VWN)
+#else
+#define STAGE_B 0
 #endif
 // Register double buffering of the shared-memory copies when their staging
 // registers (per thread) stay small.
-#define STAGE_REGS ((SA ? KWA * MVA * VWM : 0) + (SB ? KWB * NVB * VWN : 0))
+#define STAGE_REGS (STAGE_A + STAGE_B)
 #define STAGE_AHEAD (STAGE_REGS <= 32)
 
-extern "C" __global__ void __launch_bounds__(NT, 1)
+// Occupancy target handed to ptxas (OCC=1, host-chosen): as many CTAs per SM
+// as an estimate of the live registers (accumulators + one A/B fragment +
+// addressing, + staging registers without DBUF) allows; OCC=0 leaves ptxas
+// the whole 255-register budget.
+#ifndef OCC
+#define OCC 0
+#define KTC_OCC_DEFAULT
+#endif
+#define EST_REGS (MWI * NWI + MWI + NWI + 40 + (DBUF ? 0 : STAGE_REGS * STAGE_AHEAD))
+#define MINB_RAW (65536 / (NT * EST_REGS))
+#define MINB (OCC == 0 || MINB_RAW < 1 ? 1 : (MINB_RAW > 16 ? 16 : MINB_RAW))
+
+extern "C" __global__ void __launch_bounds__(NT, MINB)
 KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float beta,
      const float* __restrict__ A, const float* __restrict__ B, const float* __restrict__ Cin,
      float* __restrict__ Cout) {
@@ -104,10 +145,10 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
     const int tid = ty * MDIMC + tx;
 #endif
 #if SA
-    float* alm = smem;  // [KWG][MWG]
+    float* alm = smem;  // [1 + DBUF][KWG][MWG]
 #endif
 #if SB
-    float* blm = smem + SA * KWG * MWG;  // [KWG][NWG]
+    float* blm = smem + SA * (1 + DBUF) * KWG * MWG;  // [1 + DBUF][KWG][NWG]
 #endif
 
     float acc[MWI][NWI];
@@ -116,18 +157,54 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
 #pragma unroll
         for (int j = 0; j < NWI; ++j) acc[i][j] = 0.0f;
 
-    // Shared-memory tiles are copied through registers by the MDIMA x KDIMA
-    // (MDIMB x KDIMB) thread re-shape.  When the staging registers are few,
-    // the NEXT K-tile's global loads are issued before computing on the
-    // current one (register double buffering), hiding their latency.
+    // Shared-memory tiles are copied by the MDIMA x KDIMA (NDIMB x KDIMB)
+    // thread re-shape.  DBUF (set by the host when two tiles fit): cp.async
+    // straight into the other buffer while this one is consumed -- one
+    // barrier per K step, no staging registers.  Otherwise the copy goes
+    // through registers; when those are few, the NEXT K-tile's global loads
+    // are issued before computing on the current one.
 #if SA
     const int la0 = tid % MDIMA, la1 = tid / MDIMA;
     const bool a_copies = (VA >= MDIMA) || (la0 < VA);
-    float ra[KWA][MVA * VWM];
+#define A_SRC(kk0, kia, mv) (A + (size_t)((kk0) + la1 * KWA + (kia)) * M + m0 + (mv) * VWM)
+#define A_DST(kia, mv) (((la1 * KWA + (kia)) * MWG) + (mv) * VWM)
+#define A_MV(mia) (STRM ? (la0 + (mia) * MDIMA) : ((mia) + la0 * MVA))
 #endif
 #if SB
     const int lb0 = tid % NDIMB, lb1 = tid / NDIMB;
     const bool b_copies = (VB >= NDIMB) || (lb0 < VB);
+#define B_SRC(kk0, kib, nv) (B + (size_t)((kk0) + lb1 * KWB + (kib)) * N + n0 + (nv) * VWN)
+#define B_DST(kib, nv) (((lb1 * KWB + (kib)) * NWG) + (nv) * VWN)
+#define B_MV(nib) (STRN ? (lb0 + (nib) * NDIMB) : ((nib) + lb0 * NVB))
+#endif
+#if DBUF
+    auto issue = [&](int kk0, int buf) {
+#if SA
+        if (a_copies) {
+#pragma unroll
+            for (int kia = 0; kia < KWA; ++kia)
+#pragma unroll
+                for (int mia = 0; mia < MVA; ++mia)
+                    cp_async<VWM>(alm + buf * KWG * MWG + A_DST(kia, A_MV(mia)), A_SRC(kk0, kia, A_MV(mia)));
+        }
+#endif
+#if SB
+        if (b_copies) {
+#pragma unroll
+            for (int kib = 0; kib < KWB; ++kib)
+#pragma unroll
+                for (int nib = 0; nib < NVB; ++nib)
+                    cp_async<VWN>(blm + buf * KWG * NWG + B_DST(kib, B_MV(nib)), B_SRC(kk0, kib, B_MV(nib)));
+        }
+#endif
+        cp_async_commit();
+    };
+    issue(0, 0);
+#elif SA || SB
+#if SA
+    float ra[KWA][MVA * VWM];
+#endif
+#if SB
     float rb[KWB][NVB * VWN];
 #endif
     auto fetch = [&](int kk0) {
@@ -136,11 +213,8 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
 #pragma unroll
             for (int kia = 0; kia < KWA; ++kia)
 #pragma unroll
-                for (int mia = 0; mia < MVA; ++mia) {
-                    const int mv = STRM ? (la0 + mia * MDIMA) : (mia + la0 * MVA);
-                    vload_g<VWM>(&ra[kia][mia * VWM],
-                                 A + (size_t)(kk0 + la1 * KWA + kia) * M + m0 + mv * VWM);
-                }
+                for (int mia = 0; mia < MVA; ++mia)
+                    vload_g<VWM>(&ra[kia][mia * VWM], A_SRC(kk0, kia, A_MV(mia)));
         }
 #endif
 #if SB
@@ -148,14 +222,10 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
 #pragma unroll
             for (int kib = 0; kib < KWB; ++kib)
 #pragma unroll
-                for (int nib = 0; nib < NVB; ++nib) {
-                    const int nv = STRN ? (lb0 + nib * NDIMB) : (nib + lb0 * NVB);
-                    vload_g<VWN>(&rb[kib][nib * VWN],
-                                 B + (size_t)(kk0 + lb1 * KWB + kib) * N + n0 + nv * VWN);
-                }
+                for (int nib = 0; nib < NVB; ++nib)
+                    vload_g<VWN>(&rb[kib][nib * VWN], B_SRC(kk0, kib, B_MV(nib)));
         }
 #endif
-        (void)kk0;
     };
     auto stash = [&]() {
 #if SA
@@ -163,10 +233,8 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
 #pragma unroll
             for (int kia = 0; kia < KWA; ++kia)
 #pragma unroll
-                for (int mia = 0; mia < MVA; ++mia) {
-                    const int mv = STRM ? (la0 + mia * MDIMA) : (mia + la0 * MVA);
-                    vstore<VWM>(alm + (la1 * KWA + kia) * MWG + mv * VWM, &ra[kia][mia * VWM]);
-                }
+                for (int mia = 0; mia < MVA; ++mia)
+                    vstore<VWM>(alm + A_DST(kia, A_MV(mia)), &ra[kia][mia * VWM]);
         }
 #endif
 #if SB
@@ -174,25 +242,33 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
 #pragma unroll
             for (int kib = 0; kib < KWB; ++kib)
 #pragma unroll
-                for (int nib = 0; nib < NVB; ++nib) {
-                    const int nv = STRN ? (lb0 + nib * NDIMB) : (nib + lb0 * NVB);
-                    vstore<VWN>(blm + (lb1 * KWB + kib) * NWG + nv * VWN, &rb[kib][nib * VWN]);
-                }
+                for (int nib = 0; nib < NVB; ++nib)
+                    vstore<VWN>(blm + B_DST(kib, B_MV(nib)), &rb[kib][nib * VWN]);
         }
 #endif
     };
-#if SA || SB
     fetch(0);
 #endif
 
+    int buf = 0;
 #pragma unroll 1
     for (int k0 = 0; k0 < K; k0 += KWG) {
-#if SA || SB
+#if DBUF
+        cp_async_wait_all();
+        __syncthreads();  // tile k0 landed; everyone is done with the other buffer
+        if (k0 + KWG < K) issue(k0 + KWG, buf ^ 1);
+#elif SA || SB
         stash();
         __syncthreads();
 #if STAGE_AHEAD
         if (k0 + KWG < K) fetch(k0 + KWG);
 #endif
+#endif
+#if SA
+        const float* at = alm + DBUF * buf * KWG * MWG;
+#endif
+#if SB
+        const float* bt = blm + DBUF * buf * KWG * NWG;
 #endif
 
 #pragma unroll 1
@@ -205,7 +281,7 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
                 for (int mi = 0; mi < MVI; ++mi) {
                     const int mv = STRM ? (tx + mi * MDIMC) : (mi + tx * MVI);
 #if SA
-                    vload<VWM>(a + mi * VWM, alm + k * MWG + mv * VWM);
+                    vload<VWM>(a + mi * VWM, at + k * MWG + mv * VWM);
 #else
                     vload_g<VWM>(a + mi * VWM, A + (size_t)(k0 + k) * M + m0 + mv * VWM);
 #endif
@@ -214,7 +290,7 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
                 for (int ni = 0; ni < NVI; ++ni) {
                     const int nv = STRN ? (ty + ni * NDIMC) : (ni + ty * NVI);
 #if SB
-                    vload<VWN>(b + ni * VWN, blm + k * NWG + nv * VWN);
+                    vload<VWN>(b + ni * VWN, bt + k * NWG + nv * VWN);
 #else
                     vload_g<VWN>(b + ni * VWN, B + (size_t)(k0 + k) * N + n0 + nv * VWN);
 #endif
@@ -225,12 +301,13 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
                     for (int j = 0; j < NWI; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
             }
         }
-#if SA || SB
+#if !DBUF && (SA || SB)
         __syncthreads();
 #if !STAGE_AHEAD
         if (k0 + KWG < K) fetch(k0 + KWG);
 #endif
 #endif
+        buf ^= 1;
     }
 
     // Epilogue: Cout = alpha * acc + beta * Cin, VWN-wide stores along N.
@@ -273,4 +350,23 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
 #undef VB
 #undef NVB
 #undef STAGE_REGS
+#undef STAGE_A
+#undef STAGE_B
 #undef STAGE_AHEAD
+#undef A_SRC
+#undef A_DST
+#undef A_MV
+#undef B_SRC
+#undef B_DST
+#undef B_MV
+#undef EST_REGS
+#undef MINB_RAW
+#undef MINB
+#ifdef KTC_OCC_DEFAULT
+#undef OCC
+#undef KTC_OCC_DEFAULT
+#endif
+#ifdef KTC_DBUF_DEFAULT
+#undef DBUF
+#undef KTC_DBUF_DEFAULT
+#endif

@@ -70,10 +70,11 @@ def test_nvrtc_compiles_conv_family_for_sm100a(built, cfg):
 @pytest.mark.parametrize("row", [(128, 128, 16, 16, 16, 1, 1, 32, 16, 1, 0, 2, 1, 8),
                                  (16, 16, 16, 8, 8, 0, 0, 8, 8, 0, 0, 1, 1, 2),
                                  (64, 32, 64, 8, 32, 1, 0, 16, 8, 0, 1, 8, 1, 2)])
-def test_nvrtc_compiles_gemm_family_for_sm100a(built, row):
+@pytest.mark.parametrize("dbuf", [0, 1])
+def test_nvrtc_compiles_gemm_family_for_sm100a(built, row, dbuf):
     names = "MWG NWG KWG MDIMC NDIMC SA SB MDIMA NDIMB STRM STRN VWM VWN KWI".split()
     cubin = K.compile_source((KERNELS / "gemm.cu").read_text(),
-                             [f"-D{k}={v}" for k, v in zip(names, row)])
+                             [f"-D{k}={v}" for k, v in zip(names, row)] + [f"-DDBUF={dbuf}"])
     assert cubin[:4] == b"\x7fELF"
 
 
