@@ -62,6 +62,8 @@ class Backend {
     virtual std::string name() const = 0;
     // Hint: `request` will be evaluated soon (compile ahead).  Optional.
     virtual void prefetch(const EvaluationRequest&) {}
+    // How many requests ahead prefetch() is worth calling (0 = no preference).
+    virtual size_t prefetch_depth() const { return 0; }
     // Device ordinal behind this backend, -1 if none.
     virtual int device() const { return -1; }
     // CLTune SetReference: binds host reference outputs so the backend can
@@ -101,6 +103,7 @@ class CudaBackend : public Backend {
 
     EvaluationResult evaluate(const EvaluationRequest& r) override;
     void prefetch(const EvaluationRequest& r) override;
+    size_t prefetch_depth() const override;
     std::string name() const override;
     int device() const override { return ordinal_; }
     bool bind_reference(const EvaluationRequest& r, const std::vector<Buffer>& outputs) override;

@@ -241,6 +241,9 @@ int ktc_backend_evaluate(ktc_backend* be, const ktc_request* req, ktc_result* ou
 /* Starts compiling req's kernel in the background NVRTC pool, so a later
  * evaluate of the same configuration finds the cubin ready. */
 int ktc_backend_prefetch(ktc_backend* be, const ktc_request* req);
+/* How many requests ahead a caller should keep prefetching so that every
+ * NVRTC pool thread has work: 2 x pool threads x configurations per program. */
+size_t ktc_backend_prefetch_depth(ktc_backend* be);
 
 /* SetReference: binds host reference outputs (one buffer per output
  * argument, in order) for the argument list of `req`.  Built-in families

@@ -174,6 +174,7 @@ _SIGS = {
     "ktc_backend_ctx": (_P, [_P]),
     "ktc_backend_evaluate": (C.c_int, [_P, C.POINTER(Request), C.POINTER(Result)]),
     "ktc_backend_prefetch": (C.c_int, [_P, C.POINTER(Request)]),
+    "ktc_backend_prefetch_depth": (C.c_size_t, [_P]),
     "ktc_backend_set_reference": (C.c_int, [_P, C.POINTER(Request), C.c_int, C.POINTER(_P),
                                             C.POINTER(C.c_size_t), C.POINTER(C.c_int)]),
     "ktc_backend_read_output": (C.c_int, [_P, C.c_int, _P, C.c_size_t]),

@@ -403,6 +403,31 @@ int refresh_custom_buffers(ktc_backend* be) {
     return KTC_OK;
 }
 
+// Problem dimensions straight from the request's scalar arguments (the
+// documented layouts of check_layout): plans need nothing else, so compiles
+// can be queued before the argument list is materialized and uploaded.
+struct Dims {
+    int X = 0, Y = 0, F = 0;  // conv
+    int M = 0, N = 0, K = 0;  // gemm
+};
+
+Dims dims_of(const ktc_request* r, Family fam) {
+    Dims d;
+    auto iv = [&](int i) { return i < r->n_args ? int(r->args[i].value) : 0; };
+    if (fam == FAM_CONV) {
+        d.X = iv(0), d.Y = iv(1), d.F = iv(2);
+    } else if (fam == FAM_GEMM || fam == FAM_GEMM_TF32) {
+        d.M = iv(0), d.N = iv(1), d.K = iv(2);
+    }
+    return d;
+}
+
+bool dims_valid(const Dims& d, Family fam) {
+    if (fam == FAM_CONV) return d.X > 0 && d.Y > 0 && d.F >= 1 && d.F % 2 == 1;
+    if (fam == FAM_GEMM || fam == FAM_GEMM_TF32) return d.M > 0 && d.N > 0 && d.K > 0;
+    return true;
+}
+
 // ---------------------------------------------------------------------------
 // Plans: configuration -> NVRTC source/defines + launch geometry.
 // Returns false with a message for configurations this device cannot run
@@ -410,7 +435,7 @@ int refresh_custom_buffers(ktc_backend* be) {
 // ---------------------------------------------------------------------------
 
 bool plan_conv(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why) {
-    const Inputs& I = *be->in;
+    const Dims I = dims_of(r, FAM_CONV);
     ParamView pv{r};
     long long XWG, YWG, XWPT, YWPT, LOCAL, VW, PAD, UNR;
     if (!pv.get("XWG", &XWG) || !pv.get("YWG", &YWG) || !pv.get("XWPT", &XWPT) ||
@@ -500,8 +525,18 @@ int gemm_occ_policy() {
     return v;
 }
 
+// Register fragment double buffering in the K loop (gemm.cu FRAG).
+// KTC_GEMM_FRAG overrides.
+int gemm_frag_policy() {
+    static const int v = [] {
+        const char* e = std::getenv("KTC_GEMM_FRAG");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why) {
-    const Inputs& I = *be->in;
+    const Dims I = dims_of(r, FAM_GEMM);
     ParamView pv{r};
     static const char* names[] = {"MWG", "NWG",  "KWG",  "MDIMC", "NDIMC", "SA",  "SB",
                                   "MDIMA", "NDIMB", "STRM", "STRN", "VWM",  "VWN", "KWI"};
@@ -550,6 +585,7 @@ bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
                       2 * size_t(tile_bytes) <= be->ctx->limits.smem_per_block_optin;
     p->config.push_back(define("DBUF", dbuf ? 1 : 0));
     p->config.push_back(define("OCC", gemm_occ_policy()));
+    p->config.push_back(define("FRAG", gemm_frag_policy()));
     p->smem = dbuf ? 2 * tile_bytes : tile_bytes;
     if (p->smem > be->ctx->limits.smem_per_block_optin) {
         *why = "needs " + std::to_string(p->smem) + " bytes of shared memory";
@@ -614,7 +650,7 @@ bool plan_custom(ktc_backend* be, const ktc_request* r, Plan* p, std::string* wh
 // TF32 tcgen05 variant (kernels/gemm_tf32.cu): one 128-thread CTA per
 // 128 x BN tile, TMA tensor maps for A (M-major) and B (N-major), SWIZZLE_128B.
 bool plan_gemm_tf32(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why) {
-    const Inputs& I = *be->in;
+    const Dims I = dims_of(r, FAM_GEMM_TF32);
     ParamView pv{r};
     long long BN, BK, STAGES;
     if (!pv.get("BN", &BN) || !pv.get("BK", &BK) || !pv.get("STAGES", &STAGES)) {
@@ -977,13 +1013,8 @@ int ktc_backend_prefetch(ktc_backend* be, const ktc_request* req) {
         const Family fam = family_of(req->kernel_name);
         std::string why;
         if (fam != FAM_CUSTOM && !check_layout(req, fam, &why)) return KTC_OK;
-        // Plans need the problem scalars only; build a light Inputs view.
-        if (!be->in || be->in->sig != signature(req)) {
-            int st = make_current(be->ctx);
-            if (st) return st;
-            st = ensure_inputs(be, req, fam);
-            if (st) return st;
-        }
+        // Plans need the problem scalars only (dims_of), not the inputs.
+        if (!dims_valid(dims_of(req, fam), fam)) return KTC_OK;
         Plan plan;
         bool ok = fam == FAM_CONV   ? plan_conv(be, req, &plan, &why)
                   : fam == FAM_GEMM ? plan_gemm(be, req, &plan, &why)
@@ -995,6 +1026,12 @@ int ktc_backend_prefetch(ktc_backend* be, const ktc_request* req) {
         set_error(e.what());
         return KTC_ERR_INVALID;
     }
+}
+
+size_t ktc_backend_prefetch_depth(ktc_backend* be) {
+    if (!be) return 0;
+    CompileService& cs = CompileService::instance();
+    return size_t(2) * size_t(cs.threads()) * size_t(cs.batch());
 }
 
 int ktc_backend_set_reference(ktc_backend* be, const ktc_request* req, int n_buffers,

@@ -193,6 +193,8 @@ void CudaBackend::prefetch(const EvaluationRequest& r) {
     ktc_backend_prefetch(be_, &v.req);
 }
 
+size_t CudaBackend::prefetch_depth() const { return ktc_backend_prefetch_depth(be_); }
+
 bool CudaBackend::bind_reference(const EvaluationRequest& r, const std::vector<Buffer>& outputs) {
     RequestView v(r);
     std::vector<const void*> ptrs;

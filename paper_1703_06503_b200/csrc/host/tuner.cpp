@@ -288,7 +288,9 @@ TuningOutcome run_tuning_sharded(const TuningJob& job, const std::vector<Backend
     std::vector<std::optional<double>> times(n);
     std::atomic<size_t> next{0}, prefetched{0};
     const size_t chunk = 4;
-    const size_t window = 64;
+    // Deep enough that every compile-pool thread has a program in flight.
+    size_t window = 64;
+    for (Backend* be : backends) window = std::max(window, be->prefetch_depth());
     std::vector<std::string> errors(backends.size());
 
     auto worker = [&](size_t w) {

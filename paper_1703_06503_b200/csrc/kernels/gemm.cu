@@ -123,11 +123,15 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // as an estimate of the live registers (accumulators + one A/B fragment +
 // addressing, + staging registers without DBUF) allows; OCC=0 leaves ptxas
 // the whole 255-register budget.
+#ifndef FRAG  // host-chosen (backend.cpp plan_gemm): register fragment double buffering
+#define FRAG 0
+#define KTC_FRAG_DEFAULT
+#endif
 #ifndef OCC
 #define OCC 0
 #define KTC_OCC_DEFAULT
 #endif
-#define EST_REGS (MWI * NWI + MWI + NWI + 40 + (DBUF ? 0 : STAGE_REGS * STAGE_AHEAD))
+#define EST_REGS (MWI * NWI + (1 + FRAG) * (MWI + NWI) + 40 + (DBUF ? 0 : STAGE_REGS * STAGE_AHEAD))
 #define MINB_RAW (65536 / (NT * EST_REGS))
 #define MINB (OCC == 0 || MINB_RAW < 1 ? 1 : (MINB_RAW > 16 ? 16 : MINB_RAW))
 
@@ -250,9 +254,39 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
     fetch(0);
 #endif
 
+    // One k-step's register fragments: MWI values of A and NWI of B, as
+    // MVI (NVI) vectors of VWM (VWN), from the staged tile or from global.
+#if SA
+    const float* at = alm;
+#endif
+#if SB
+    const float* bt = blm;
+#endif
+    int k0 = 0;
+    auto load_frag = [&](float* a, float* b, int k) {
+#pragma unroll
+        for (int mi = 0; mi < MVI; ++mi) {
+            const int mv = STRM ? (tx + mi * MDIMC) : (mi + tx * MVI);
+#if SA
+            vload<VWM>(a + mi * VWM, at + k * MWG + mv * VWM);
+#else
+            vload_g<VWM>(a + mi * VWM, A + (size_t)(k0 + k) * M + m0 + mv * VWM);
+#endif
+        }
+#pragma unroll
+        for (int ni = 0; ni < NVI; ++ni) {
+            const int nv = STRN ? (ty + ni * NDIMC) : (ni + ty * NVI);
+#if SB
+            vload<VWN>(b + ni * VWN, bt + k * NWG + nv * VWN);
+#else
+            vload_g<VWN>(b + ni * VWN, B + (size_t)(k0 + k) * N + n0 + nv * VWN);
+#endif
+        }
+    };
+
     int buf = 0;
 #pragma unroll 1
-    for (int k0 = 0; k0 < K; k0 += KWG) {
+    for (k0 = 0; k0 < K; k0 += KWG) {
 #if DBUF
         cp_async_wait_all();
         __syncthreads();  // tile k0 landed; everyone is done with the other buffer
@@ -265,42 +299,44 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
 #endif
 #endif
 #if SA
-        const float* at = alm + DBUF * buf * KWG * MWG;
+        at = alm + DBUF * buf * KWG * MWG;
 #endif
 #if SB
-        const float* bt = blm + DBUF * buf * KWG * NWG;
+        bt = blm + DBUF * buf * KWG * NWG;
 #endif
 
+#if FRAG
+        // Register fragments double-buffered across k: the A/B vectors of
+        // step k+1 are loaded while the outer product of step k runs (the
+        // next tile's first fragment is loaded after its barrier, above).
+        float fa[2][MWI], fb[2][NWI];
+        load_frag(fa[0], fb[0], 0);
 #pragma unroll 1
         for (int kw = 0; kw < KWG; kw += KWI) {
 #pragma unroll
             for (int ki = 0; ki < KWI; ++ki) {
                 const int k = kw + ki;
+                if (ki + 1 < KWI || kw + KWI < KWG) load_frag(fa[(ki + 1) & 1], fb[(ki + 1) & 1], k + 1);
+#pragma unroll
+                for (int i = 0; i < MWI; ++i)
+#pragma unroll
+                    for (int j = 0; j < NWI; ++j) acc[i][j] = fmaf(fa[ki & 1][i], fb[ki & 1][j], acc[i][j]);
+            }
+        }
+#else
+#pragma unroll 1
+        for (int kw = 0; kw < KWG; kw += KWI) {
+#pragma unroll
+            for (int ki = 0; ki < KWI; ++ki) {
                 float a[MWI], b[NWI];
-#pragma unroll
-                for (int mi = 0; mi < MVI; ++mi) {
-                    const int mv = STRM ? (tx + mi * MDIMC) : (mi + tx * MVI);
-#if SA
-                    vload<VWM>(a + mi * VWM, at + k * MWG + mv * VWM);
-#else
-                    vload_g<VWM>(a + mi * VWM, A + (size_t)(k0 + k) * M + m0 + mv * VWM);
-#endif
-                }
-#pragma unroll
-                for (int ni = 0; ni < NVI; ++ni) {
-                    const int nv = STRN ? (ty + ni * NDIMC) : (ni + ty * NVI);
-#if SB
-                    vload<VWN>(b + ni * VWN, bt + k * NWG + nv * VWN);
-#else
-                    vload_g<VWN>(b + ni * VWN, B + (size_t)(k0 + k) * N + n0 + nv * VWN);
-#endif
-                }
+                load_frag(a, b, kw + ki);
 #pragma unroll
                 for (int i = 0; i < MWI; ++i)
 #pragma unroll
                     for (int j = 0; j < NWI; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
             }
         }
+#endif
 #if !DBUF && (SA || SB)
         __syncthreads();
 #if !STAGE_AHEAD
@@ -365,6 +401,10 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
 #ifdef KTC_OCC_DEFAULT
 #undef OCC
 #undef KTC_OCC_DEFAULT
+#endif
+#ifdef KTC_FRAG_DEFAULT
+#undef FRAG
+#undef KTC_FRAG_DEFAULT
 #endif
 #ifdef KTC_DBUF_DEFAULT
 #undef DBUF

@@ -17,6 +17,7 @@ namespace ktc {
 namespace {
 
 const char* kMarker = "//@@KTC_BODY@@";
+const char* kDefaultFastCompile = "0";
 
 uint64_t fnv(const std::string& s, uint64_t h = 0xcbf29ce484222325ull) {
     for (unsigned char c : s) {
@@ -36,9 +37,19 @@ std::string hash_name(const std::string& key) {
     return hex64(fnv(key)) + hex64(fnv(key, 0x84222325cbf29ce4ull));
 }
 
+// Options every tuning-time compile gets.  KTC_LINEINFO=1 adds -lineinfo
+// (profiling runs: ncu source page); KTC_FAST_COMPILE=<0|min|mid|max>
+// selects NVRTC's --Ofast-compile level.  Both are part of the cache key.
 const std::vector<std::string>& base_options() {
-    static const std::vector<std::string> opts = {"--gpu-architecture=sm_100a", "--std=c++17",
-                                                  "-lineinfo", "--fmad=true"};
+    static const std::vector<std::string> opts = [] {
+        std::vector<std::string> o = {"--gpu-architecture=sm_100a", "--std=c++17", "--fmad=true"};
+        const char* li = std::getenv("KTC_LINEINFO");
+        if (li && std::strcmp(li, "0") != 0) o.push_back("-lineinfo");
+        const char* fc = std::getenv("KTC_FAST_COMPILE");
+        const std::string level = fc ? fc : kDefaultFastCompile;
+        if (!level.empty() && level != "0") o.push_back("--Ofast-compile=" + level);
+        return o;
+    }();
     return opts;
 }
 
@@ -246,6 +257,39 @@ void CompileService::run_batch(Batch b) {
         for (Item* it : all) compile_group({it});  // attribute errors to their configuration
 }
 
+// Work-conserving batching: a batch taken while other pool threads sit idle
+// (and no other batch is waiting for them) is split so they share it.  Full
+// batches amortize NVRTC's fixed cost when the pool is saturated; on a burst
+// into an idle pool (a fresh job, the head of a search) smaller programs
+// finish sooner, and the first configurations -- kept by this thread --
+// are the ones the evaluator needs first.
+void CompileService::split_for_idle_locked(Batch& b) {
+    if (!b.src || !b.src->batchable || b.items.size() < 2) return;
+    const size_t spare = size_t(idle_) > ready_.size() ? size_t(idle_) - ready_.size() : 0;
+    if (spare == 0) return;
+    const size_t parts = std::min(spare + 1, b.items.size());
+    const size_t keep = (b.items.size() + parts - 1) / parts;
+    Batch rest;
+    rest.src = b.src;
+    rest.problem = b.problem;
+    rest.born = b.born;
+    rest.items.assign(std::make_move_iterator(b.items.begin() + keep),
+                      std::make_move_iterator(b.items.end()));
+    b.items.resize(keep);
+    ready_.push_front(std::move(rest));
+    cv_.notify_one();
+}
+
+int CompileService::threads() {
+    std::lock_guard<std::mutex> lk(mu_);
+    return want_threads_ > 0 ? want_threads_ : int(std::max(1u, std::thread::hardware_concurrency()));
+}
+
+int CompileService::batch() {
+    std::lock_guard<std::mutex> lk(mu_);
+    return batch_;
+}
+
 void CompileService::worker() {
     using namespace std::chrono;
     for (;;) {
@@ -256,6 +300,7 @@ void CompileService::worker() {
                 if (!ready_.empty()) {
                     b = std::move(ready_.front());
                     ready_.pop_front();
+                    split_for_idle_locked(b);
                     break;
                 }
                 // A partially filled batch is taken once it has waited a
@@ -267,9 +312,12 @@ void CompileService::worker() {
                     steady_clock::now() - oldest->second.born > milliseconds(10)) {
                     b = std::move(oldest->second);
                     pending_.erase(oldest);
+                    split_for_idle_locked(b);
                     break;
                 }
+                ++idle_;
                 cv_.wait_for(lk, milliseconds(oldest == pending_.end() ? 100 : 3));
+                --idle_;
             }
         }
         run_batch(std::move(b));

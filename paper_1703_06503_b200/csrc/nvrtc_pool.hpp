@@ -82,6 +82,8 @@ class CompileService {
                   bool* hit);
     void prefetch(const KernelSource& src, const Defines& problem, const Defines& config);
 
+    int threads();
+    int batch();
     double total_compile_ms();
     size_t programs_compiled();
     void reset_stats();
@@ -102,6 +104,7 @@ class CompileService {
     std::string key_of(const KernelSource& src, const Defines& problem, const Defines& config) const;
     std::string batch_key_of(const KernelSource& src, const Defines& problem) const;
     void run_batch(Batch b);
+    void split_for_idle_locked(Batch& b);
     void worker();
     void ensure_workers_locked();
     // Registers `config` (if new) in the pending batch of its key; returns
@@ -120,6 +123,7 @@ class CompileService {
     std::vector<std::thread> workers_;
     int want_threads_ = 0;
     int batch_ = 8;
+    int idle_ = 0;  // pool threads waiting for work
     std::string cache_dir_;
     double compile_ms_ = 0.0;
     size_t programs_ = 0;
