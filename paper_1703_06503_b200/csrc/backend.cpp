@@ -434,6 +434,15 @@ bool dims_valid(const Dims& d, Family fam) {
 // (reported as runtime_error, like a launch failure).
 // ---------------------------------------------------------------------------
 
+// Row-paired FFMA2 in the unrolled conv (conv.cu CF2); KTC_CONV_F2 overrides.
+int conv_f2_policy() {
+    static const int v = [] {
+        const char* e = std::getenv("KTC_CONV_F2");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 bool plan_conv(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why) {
     const Dims I = dims_of(r, FAM_CONV);
     ParamView pv{r};
@@ -459,7 +468,7 @@ bool plan_conv(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
          define("YWPT", YWPT), define("LOCAL", LOCAL), define("VW", VW),
          define("PAD", LOCAL >= 1 ? PAD : 0), define("UNR", UNR ? 1 : 0),
          define("GUARD", (I.X % TX != 0 || I.Y % TY != 0) ? 1 : 0),
-         define("OUT_VEC", I.X % VW == 0 ? 1 : 0)};
+         define("OUT_VEC", I.X % VW == 0 ? 1 : 0), define("CF2", conv_f2_policy())};
     size_t smem_floats = 0;
     if (LOCAL == 1) {
         const long long SP = TX + 2 * H + PAD;
@@ -535,6 +544,15 @@ int gemm_frag_policy() {
     return v;
 }
 
+// Packed FFMA2 outer products (gemm.cu F2); KTC_GEMM_F2 overrides.
+int gemm_f2_policy() {
+    static const int v = [] {
+        const char* e = std::getenv("KTC_GEMM_F2");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why) {
     const Dims I = dims_of(r, FAM_GEMM);
     ParamView pv{r};
@@ -586,6 +604,7 @@ bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
     p->config.push_back(define("DBUF", dbuf ? 1 : 0));
     p->config.push_back(define("OCC", gemm_occ_policy()));
     p->config.push_back(define("FRAG", gemm_frag_policy()));
+    p->config.push_back(define("F2", gemm_f2_policy()));
     p->smem = dbuf ? 2 * tile_bytes : tile_bytes;
     if (p->smem > be->ctx->limits.smem_per_block_optin) {
         *why = "needs " + std::to_string(p->smem) + " bytes of shared memory";
@@ -780,6 +799,22 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
             if (ktc_set_symbol(fn, "c_taps", I.taps.data(), I.taps.size() * 4) != KTC_OK) {
                 set_msg(out, last_error());
                 return ctx->sticky ? KTC_ERR_LAUNCH : KTC_OK;
+            }
+            // Row-paired taps (conv.cu c_tpair), when the module kept the symbol.
+            CUdeviceptr tp = 0;
+            size_t tp_size = 0;
+            if (d.cuModuleGetGlobal(&tp, &tp_size, fn->mod, "c_tpair") == CUDA_SUCCESS) {
+                std::vector<float> pairs(size_t(2) * I.F * I.F, 0.0f);
+                for (int jj = 1; jj < I.F; ++jj)
+                    for (int i = 0; i < I.F; ++i) {
+                        pairs[2 * size_t(jj * I.F + i)] = I.taps[size_t(jj * I.F + i)];
+                        pairs[2 * size_t(jj * I.F + i) + 1] = I.taps[size_t((jj - 1) * I.F + i)];
+                    }
+                if (tp_size < pairs.size() * 4 ||
+                    d.cuMemcpyHtoD(tp, pairs.data(), pairs.size() * 4) != CUDA_SUCCESS) {
+                    set_msg(out, "cannot set c_tpair");
+                    return ctx->sticky ? KTC_ERR_LAUNCH : KTC_OK;
+                }
             }
             me->taps_sig = I.sig;
         }

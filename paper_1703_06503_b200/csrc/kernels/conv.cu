@@ -24,6 +24,7 @@
 //                  constant-bank operands of FFMA);
 //               0: filter loops rolled (#pragma unroll 1)
 //   FS          filter size (compile-time)
+//   CF2         (host) 1: UNR=1 pairs output rows into packed FFMA2 (c_tpair)
 //   GUARD       1 when X % (XWG*XWPT) or Y % (YWG*YWPT) is non-zero
 // Derived (host-computed): SP (LOCAL=1 pitch), PWO/BW/BH/NB/NP/PF (LOCAL=2
 // panel geometry: PWO output columns per panel, box BW x BH floats, NB boxes
@@ -32,6 +33,9 @@
 typedef unsigned int u32;
 
 __constant__ float c_taps[FS * FS];
+// Tap pairs for row-paired FFMA2: c_tpair[jj*FS + i] = (taps[jj][i], taps[jj-1][i]),
+// jj >= 1 (set by the host next to c_taps).
+__constant__ float2 c_tpair[FS * FS];
 
 struct __align__(64) TensorMap {
     unsigned long long v[16];
@@ -134,6 +138,10 @@ __device__ __forceinline__ void tma_load_2d(u32 dst, const TensorMap* map, u32 b
 //@@KTC_BODY@@ -- everything below is instantiated once per configuration
 // (inside its own namespace when several configurations share one NVRTC
 // program); KTC_ENTRY names the kernel.
+#ifndef CF2  // host-chosen (backend.cpp plan_conv): row-paired FFMA2
+#define CF2 1
+#define KTC_CF2_DEFAULT
+#endif
 #define H ((FS - 1) / 2)
 #define TX (XWG * XWPT)
 #define TY (YWG * YWPT)
@@ -248,6 +256,40 @@ KTC_ENTRY(const int X, const int Y, const float W, const float* __restrict__ img
                 ld_shared<SVW>(w + v * SVW, rp + v * SVW);
 #endif
             }
+#if CF2 && YWPT % 2 == 0
+            // Output rows j, j+1 read input row r through tap rows jj, jj-1:
+            // one packed FFMA2 per (tap pair, column) with the input value
+            // broadcast -- half the FMA-pipe instructions, each lane an exact
+            // fmaf, the same per-output order (jj, i ascending) as below.
+            // Tap rows outside [0, FS) leave single rows: scalar FFMA.
+#pragma unroll
+            for (int j = 0; j < YWPT; j += 2) {
+                const int jj = r - j;
+                if (jj >= 1 && jj < FS) {
+#pragma unroll
+                    for (int i = 0; i < FS; ++i) {
+                        const float2 t2 = c_tpair[jj * FS + i];
+#pragma unroll
+                        for (int e = 0; e < VW; ++e) {
+                            const float2 q = __ffma2_rn(t2, make_float2(w[e + i], w[e + i]),
+                                                        make_float2(acc[j][g * VW + e], acc[j + 1][g * VW + e]));
+                            acc[j][g * VW + e] = q.x;
+                            acc[j + 1][g * VW + e] = q.y;
+                        }
+                    }
+                } else if (jj == 0 || jj == FS) {
+                    const int jr = jj == 0 ? j : j + 1;  // the row that has a tap row
+                    const int jt = jj == 0 ? 0 : FS - 1;
+#pragma unroll
+                    for (int i = 0; i < FS; ++i) {
+                        const float t = c_taps[jt * FS + i];
+#pragma unroll
+                        for (int e = 0; e < VW; ++e)
+                            acc[jr][g * VW + e] = fmaf(t, w[e + i], acc[jr][g * VW + e]);
+                    }
+                }
+            }
+#else
 #pragma unroll
             for (int j = 0; j < YWPT; ++j) {
                 const int jj = r - j;
@@ -261,6 +303,7 @@ KTC_ENTRY(const int X, const int Y, const float W, const float* __restrict__ img
                     }
                 }
             }
+#endif
         }
     }
 #else
@@ -332,3 +375,7 @@ KTC_ENTRY(const int X, const int Y, const float W, const float* __restrict__ img
 #undef WIN
 #undef NWV
 #undef WINP
+#ifdef KTC_CF2_DEFAULT
+#undef CF2
+#undef KTC_CF2_DEFAULT
+#endif

@@ -85,6 +85,42 @@ __device__ __forceinline__ void cp_async(float* s, const float* __restrict__ g) 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// acc[i][j] += a[i] * b[j] over an MI x NJ register tile.  PAIRED: the
+// Blackwell packed FP32 FMA (FFMA2, fma.rn.f32x2): two independent
+// round-to-nearest FMAs per instruction with one operand broadcast, so each
+// lane's result is bit-identical to fmaf while the FMA-pipe issue count
+// halves -- the SIMT SGEMM is issue-bound without it.  Pairs run along j
+// (NJ even), else along i (MI even), else scalar.
+template <int MI, int NJ, bool PAIRED>
+__device__ __forceinline__ void outer_product_t(float (&acc)[MI][NJ], const float* a, const float* b) {
+    if (PAIRED && NJ % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int j = 0; j < NJ; j += 2) {
+                const float2 r = __ffma2_rn(make_float2(a[i], a[i]), make_float2(b[j], b[j + 1]),
+                                            make_float2(acc[i][j], acc[i][j + 1]));
+                acc[i][j] = r.x;
+                acc[i][j + 1] = r.y;
+            }
+    } else if (PAIRED && MI % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < MI; i += 2)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                const float2 r = __ffma2_rn(make_float2(a[i], a[i + 1]), make_float2(b[j], b[j]),
+                                            make_float2(acc[i][j], acc[i + 1][j]));
+                acc[i][j] = r.x;
+                acc[i + 1][j] = r.y;
+            }
+    } else {
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+}
+
 //@@KTC_BODY@@ -- instantiated once per configuration; KTC_ENTRY names the kernel.
 #ifndef DBUF  // host-chosen (backend.cpp plan_gemm): double-buffered cp.async tiles
 #define DBUF 0
@@ -127,6 +163,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #define FRAG 0
 #define KTC_FRAG_DEFAULT
 #endif
+#ifndef F2  // host-chosen: packed FFMA2 outer products
+#define F2 1
+#define KTC_F2_DEFAULT
+#endif
+#define outer_product(acc, a, b) outer_product_t<MWI, NWI, (F2 != 0)>(acc, a, b)
 #ifndef OCC
 #define OCC 0
 #define KTC_OCC_DEFAULT
@@ -317,10 +358,7 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
             for (int ki = 0; ki < KWI; ++ki) {
                 const int k = kw + ki;
                 if (ki + 1 < KWI || kw + KWI < KWG) load_frag(fa[(ki + 1) & 1], fb[(ki + 1) & 1], k + 1);
-#pragma unroll
-                for (int i = 0; i < MWI; ++i)
-#pragma unroll
-                    for (int j = 0; j < NWI; ++j) acc[i][j] = fmaf(fa[ki & 1][i], fb[ki & 1][j], acc[i][j]);
+                outer_product(acc, fa[ki & 1], fb[ki & 1]);
             }
         }
 #else
@@ -330,10 +368,7 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
             for (int ki = 0; ki < KWI; ++ki) {
                 float a[MWI], b[NWI];
                 load_frag(a, b, kw + ki);
-#pragma unroll
-                for (int i = 0; i < MWI; ++i)
-#pragma unroll
-                    for (int j = 0; j < NWI; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+                outer_product(acc, a, b);
             }
         }
 #endif
@@ -401,6 +436,11 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
 #ifdef KTC_OCC_DEFAULT
 #undef OCC
 #undef KTC_OCC_DEFAULT
+#endif
+#undef outer_product
+#ifdef KTC_F2_DEFAULT
+#undef F2
+#undef KTC_F2_DEFAULT
 #endif
 #ifdef KTC_FRAG_DEFAULT
 #undef FRAG

@@ -28,6 +28,10 @@ def main():
             f = int(w[4:])
             cfg = table["conv"][str(f)]["config"]
             r = be.evaluate(pkg.conv_request(8192, 4096, f, pkg.parse_canonical(cfg), reps=2))
+        elif w.startswith("gemm:"):  # gemm:<size>:<canonical config>
+            _, size, cfg = w.split(":", 2)
+            m = int(size)
+            r = be.evaluate(pkg.gemm_request(m, m, m, pkg.parse_canonical(cfg), reps=2))
         elif w == "gemm":
             cfg = table["gemm"]["2048"]["config"]
             r = be.evaluate(pkg.gemm_request(2048, 2048, 2048, pkg.parse_canonical(cfg), reps=2))
