@@ -97,3 +97,44 @@ def test_digest_matches_reference_format(built):
     from oracle import oracle as O
 
     assert buf.value.decode() == O.digest(a)
+
+
+def _sass(cubin: bytes, tmp_path) -> str:
+    import shutil
+    import subprocess
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not Path(tool).exists():
+        pytest.skip("cuobjdump not available")
+    p = tmp_path / "k.cubin"
+    p.write_bytes(cubin)
+    return subprocess.run([tool, "-sass", str(p)], capture_output=True, text=True, check=True).stdout
+
+
+@pytest.mark.parametrize("f2", [0, 1])
+def test_gemm_outer_product_issues_packed_ffma2(built, tmp_path, f2):
+    """F2=1 (the default): the 8x8 register tile is 32 FFMA2 per k step, not 64 FFMA."""
+    names = "MWG NWG KWG MDIMC NDIMC SA SB MDIMA NDIMB STRM STRN VWM VWN KWI".split()
+    row = (128, 128, 32, 16, 16, 1, 1, 16, 16, 1, 1, 4, 4, 8)
+    cubin = K.compile_source((KERNELS / "gemm.cu").read_text(),
+                             [f"-D{k}={v}" for k, v in zip(names, row)] + ["-DDBUF=1", f"-DF2={f2}"])
+    sass = _sass(cubin, tmp_path)
+    n2 = len(re.findall(r"\bFFMA2\b", sass))
+    n1 = len(re.findall(r"\bFFMA\b", sass))
+    if f2:
+        assert n2 == 8 * 64 // 2 and n1 <= 64  # KWI=8 steps x 64 FMAs, paired; scalar only in the beta epilogue
+    else:
+        assert n2 == 0 and n1 >= 8 * 64
+
+
+def test_conv_unrolled_rows_issue_packed_ffma2(built, tmp_path):
+    """CF2=1 (default): 11x11 taps, YWPT=4 rows pair into FFMA2; edge tap rows stay scalar."""
+    opts = _conv_defines(11, 16, 8, 4, 4, 2, 4, 0, 1)
+    sass = _sass(K.compile_source((KERNELS / "conv.cu").read_text(), opts), tmp_path)
+    n2 = len(re.findall(r"\bFFMA2\b", sass))
+    n1 = len(re.findall(r"\bFFMA\b", sass))
+    # 4 rows x 121 taps x 4 columns = 1936 FMAs: 2 row pairs x 10 inner tap rows
+    # x 11 x 4 = 880 FFMA2 and 2 x 2 edge rows x 11 x 4 = 176 FFMA.
+    assert (n2, n1) == (880, 176)
+    sass0 = _sass(K.compile_source((KERNELS / "conv.cu").read_text(), opts + ["-DCF2=0"]), tmp_path)
+    assert len(re.findall(r"\bFFMA2\b", sass0)) == 0

@@ -23,6 +23,16 @@ ap.add_argument("--filter", type=int, default=3)
 a = ap.parse_args()
 order = list(range(5104))
 random.Random(99).shuffle(order)
+reuse = pkg.Tuner.conv(8192, 4096, a.filter, devices=[0])
+reuse.SetVerification(True)
+reuse.SetRepetitions(3)
+for j in range(a.jobs):
+    reuse.SetSubset(order[(50 + j) * a.chunk:(51 + j) * a.chunk])
+    t0 = time.perf_counter()
+    s = reuse.Tune()
+    t1 = time.perf_counter()
+    print(f"same tuner, new units {j}: Tune {1e3 * (t1 - t0):.1f} ms (compile {s['compile_s']:.2f} s "
+          f"summed, device {s['device_s']:.3f} s) -> {a.chunk / (t1 - t0):.1f} configs/s", flush=True)
 for j in range(a.jobs):
     t0 = time.perf_counter()
     t = pkg.Tuner.conv(8192, 4096, a.filter, devices=[0])
