@@ -17,7 +17,9 @@
 #include <cmath>
 #include <cstring>
 #include <fstream>
+#include <algorithm>
 #include <map>
+#include <set>
 #include <memory>
 #include <mutex>
 #include <sstream>
@@ -76,7 +78,14 @@ struct Plan {
     int tma_mode = 0;  // 1: conv halo tile box (BW x BH); 2: tf32 A/B operand boxes
     double rel_tol = -1.0;  // family tolerance override (< 0: backend options)
     unsigned box[2] = {0, 0};
+    double compile_cost = 1.0;  // relative NVRTC cost estimate (CompileService ordering)
 };
+
+// Relative NVRTC cost of a kernel whose fully unrolled body holds `n` FMAs
+// per thread (1 ~ 100 ms on the GPU box).  NVVM's optimizer grows
+// super-linearly with the unrolled body (measured: 11x11 taps with 8x8
+// outputs/thread, 7,744 FMAs, ~6.9 s; 3x3 with 8x8, 576, ~0.45 s).
+double unrolled_cost(double n) { return 1.0 + n / 200.0 + (n / 2000.0) * (n / 2000.0); }
 
 std::string define(const char* name, long long v) {
     return std::string(name) + "=" + std::to_string(v);
@@ -214,25 +223,40 @@ bool check_layout(const ktc_request* r, Family fam, std::string* why) {
 // Host copies of materialized recipes, in pinned memory, shared by every
 // backend of the process: a job's inputs are a pure function of their recipe
 // (arguments.hpp:126-180), so a new job over the same problem only pays the
-// H2D copy.  Bounded (LRU by insertion) to 4 GiB.
+// H2D copy.  Bounded (LRU by insertion) to 4 GiB.  Pinned allocations die
+// with the context that made them, so the cache holds its own retain on
+// that device's primary context (a job that closes the last backend must
+// not free them under the cache) and drops entries made before a
+// primary-context reset (primary_ctx_epoch).
 struct PinnedInput {
     void* host = nullptr;
     size_t bytes = 0;
+    unsigned epoch = 0;
     ~PinnedInput() {
-        if (host) driver().cuMemFreeHost(host);
+        if (host && epoch == primary_ctx_epoch()) driver().cuMemFreeHost(host);
     }
 };
 
-std::shared_ptr<PinnedInput> pinned_recipe(const ktb::ArgumentSpec& a) {
+std::shared_ptr<PinnedInput> pinned_recipe(const ktb::ArgumentSpec& a, CUdevice dev) {
     static std::mutex mu;
     static std::vector<std::pair<std::string, std::shared_ptr<PinnedInput>>> cache;
+    static std::set<int> retained;  // devices whose primary context the cache keeps alive
     const std::string key = std::string(ktb::to_string(a.type)) + "|" + a.fill + "|" +
                             std::to_string(a.length);
     std::lock_guard<std::mutex> lk(mu);
+    const unsigned epoch = primary_ctx_epoch();
+    cache.erase(std::remove_if(cache.begin(), cache.end(),
+                               [&](const auto& e) { return e.second->epoch != epoch; }),
+                cache.end());
     for (auto& e : cache)
         if (e.first == key) return e.second;
+    if (retained.insert(int(dev)).second) {
+        CUcontext keep = nullptr;
+        driver().cuDevicePrimaryCtxRetain(&keep, dev);  // released at process exit
+    }
     auto p = std::make_shared<PinnedInput>();
     p->bytes = a.length * 4;
+    p->epoch = epoch;
     if (driver().cuMemHostAlloc(&p->host, p->bytes ? p->bytes : 4, CU_MEMHOSTALLOC_PORTABLE) !=
         CUDA_SUCCESS) {
         p->host = nullptr;
@@ -287,7 +311,7 @@ int build_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
         // and every row start is 16-byte aligned for float4 / TMA.
         I.ipitch = int(round_up(round_up(size_t(I.X), 512) + I.F + 8, 64));
         I.rows = int(round_up(size_t(I.Y), 512) + I.F + 32);
-        std::shared_ptr<PinnedInput> img = pinned_recipe(I.args[4]);
+        std::shared_ptr<PinnedInput> img = pinned_recipe(I.args[4], ctx->dev);
         I.taps.resize(size_t(I.F) * I.F);
         ktb::materialize_into(I.args[5], I.taps.data());
         I.bytes[4] = size_t(I.ipitch) * I.rows * 4;
@@ -317,7 +341,7 @@ int build_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
             return KTC_ERR_INVALID;
         }
         for (int a = 5; a <= 7; ++a) {  // A, B, C (C pristine: kernels write a separate output)
-            std::shared_ptr<PinnedInput> h = pinned_recipe(I.args[a]);
+            std::shared_ptr<PinnedInput> h = pinned_recipe(I.args[a], ctx->dev);
             I.bytes[a] = h->bytes;
             CK(alloc(I.bytes[a], &I.dev[a]), "cuMemAlloc(matrix)");
             CK(d.cuMemcpyHtoD(I.dev[a], h->host, I.bytes[a]), "cuMemcpyHtoD(matrix)");
@@ -379,8 +403,10 @@ int ensure_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
     if (be->in && be->in->sig == sig) return KTC_OK;
     free_inputs(be);
     int st;
+    const auto t0 = std::chrono::steady_clock::now();
     try {
         st = build_inputs(be, r, fam);
+        trace_phase("build inputs (+reference)", t0);
     } catch (const std::exception& e) {
         set_error(e.what());
         st = KTC_ERR_INVALID;
@@ -490,6 +516,7 @@ bool plan_conv(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
         p->box[1] = unsigned(BH);
     }
     p->smem = unsigned(smem_floats * 4);
+    p->compile_cost = unrolled_cost(double(XWPT * YWPT) * (UNR ? double(I.F) * I.F : 4.0));
     if (p->smem > be->ctx->limits.smem_per_block_optin) {
         *why = "needs " + std::to_string(p->smem) + " bytes of shared memory; the device allows " +
                std::to_string(be->ctx->limits.smem_per_block_optin);
@@ -606,6 +633,7 @@ bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
     p->config.push_back(define("FRAG", gemm_frag_policy()));
     p->config.push_back(define("F2", gemm_f2_policy()));
     p->smem = dbuf ? 2 * tile_bytes : tile_bytes;
+    p->compile_cost = unrolled_cost(double((MWG / MDIMC) * (NWG / NDIMC) * KWI) + 64.0);
     if (p->smem > be->ctx->limits.smem_per_block_optin) {
         *why = "needs " + std::to_string(p->smem) + " bytes of shared memory";
         return false;
@@ -735,7 +763,8 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
     // 1. cubin
     auto t0 = Clock::now();
     bool hit = false;
-    KernelPtr kern = CompileService::instance().get(*plan.ksrc, plan.problem, plan.config, &hit);
+    KernelPtr kern =
+        CompileService::instance().get(*plan.ksrc, plan.problem, plan.config, &hit, plan.compile_cost);
     out->compile_ms = hit ? 0.0 : ms_since(t0);
     out->compile_cache_hit = hit ? 1 : 0;
     if (!kern->ok()) {
@@ -1019,13 +1048,17 @@ int ktc_backend_open(int ordinal, const ktc_backend_options* opts, ktc_backend**
 
 void ktc_backend_close(ktc_backend* be) {
     if (!be) return;
+    const auto t0 = std::chrono::steady_clock::now();
     free_inputs(be);
+    trace_phase("close: free inputs", t0);
     if (!be->ctx->sticky) {
         driver().cuCtxSetCurrent(be->ctx->cu);
         for (ModuleEntry& m : be->modules) driver().cuModuleUnload(m.mod);
     }
+    trace_phase("close: + module unloads", t0);
     be->modules.clear();
     ktc_close(be->ctx);
+    trace_phase("close: + context", t0);
     delete be;
 }
 
@@ -1055,7 +1088,9 @@ int ktc_backend_prefetch(ktc_backend* be, const ktc_request* req) {
                   : fam == FAM_GEMM ? plan_gemm(be, req, &plan, &why)
                   : fam == FAM_GEMM_TF32 ? plan_gemm_tf32(be, req, &plan, &why)
                                          : plan_custom(be, req, &plan, &why);
-        if (ok) CompileService::instance().prefetch(*plan.ksrc, plan.problem, plan.config);
+        if (ok)
+            CompileService::instance().prefetch(*plan.ksrc, plan.problem, plan.config,
+                                                plan.compile_cost);
         return KTC_OK;
     } catch (const std::exception& e) {
         set_error(e.what());

@@ -1,7 +1,10 @@
 // core.cpp -- ktc.h layer 1: device primitives over the CUDA driver API.
 #include "core.hpp"
 
+#include <atomic>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -281,9 +284,28 @@ static int setup_ctx(ktc_ctx* c) {
     return KTC_OK;
 }
 
+static std::atomic<unsigned> g_primary_epoch{0};
+}  // extern "C"
+unsigned ktc::primary_ctx_epoch() { return g_primary_epoch.load(); }
+bool ktc::trace_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("KTC_TRACE");
+        return e && std::strcmp(e, "0") != 0;
+    }();
+    return on;
+}
+void ktc::trace_phase(const char* what, std::chrono::steady_clock::time_point since) {
+    if (!trace_on()) return;
+    const double ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - since).count();
+    std::fprintf(stderr, "ktc-trace %-28s %9.2f ms\n", what, ms);
+}
+extern "C" {
+
 static void teardown_ctx(ktc_ctx* c, bool reset) {
     const Driver& d = driver();
     if (!c->cu) return;
+    const auto t0 = std::chrono::steady_clock::now();
     d.cuCtxSetCurrent(c->cu);
     if (!reset) {
         for (CUevent e : c->events) d.cuEventDestroy(e);
@@ -299,8 +321,13 @@ static void teardown_ctx(ktc_ctx* c, bool reset) {
     c->stream = nullptr;
     c->ref = 0;
     c->ref_count = 0;
-    if (reset) d.cuDevicePrimaryCtxReset(c->dev);
+    ktc::trace_phase("teardown: frees", t0);
+    if (reset) {
+        d.cuDevicePrimaryCtxReset(c->dev);
+        g_primary_epoch.fetch_add(1);
+    }
     else d.cuDevicePrimaryCtxRelease(c->dev);
+    ktc::trace_phase("teardown: + ctx release", t0);
     c->cu = nullptr;
 }
 

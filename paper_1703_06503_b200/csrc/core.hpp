@@ -3,6 +3,8 @@
 
 #include <cuda.h>
 
+#include <chrono>
+
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -55,6 +57,14 @@ namespace ktc {
 // Thread-local last-error plumbing shared by every layer.
 void set_error(const std::string& msg);
 const std::string& last_error();
+
+// KTC_TRACE=1: phase timings of job setup / teardown on stderr (diagnostics).
+bool trace_on();
+void trace_phase(const char* what, std::chrono::steady_clock::time_point since);
+
+// Bumped whenever a primary context is reset (destroyed): host allocations
+// tied to the old context (pinned recipe copies) are gone with it.
+unsigned primary_ctx_epoch();
 
 // Records `rc` on ctx (marking sticky errors) and returns a ktc.h code.
 int fail_cu(ktc_ctx* ctx, CUresult rc, const char* what);

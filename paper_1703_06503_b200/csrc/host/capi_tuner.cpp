@@ -17,6 +17,7 @@
 
 namespace ktc {
 void set_error(const std::string& msg);
+void trace_phase(const char* what, std::chrono::steady_clock::time_point since);
 }
 
 using namespace ktb;
@@ -507,8 +508,11 @@ void ensure_backends(ktc_tuner* t) {
 }
 
 void tune(ktc_tuner* t) {
+    const auto tb = std::chrono::steady_clock::now();
     ensure_backends(t);
+    ktc::trace_phase("tune: backends", tb);
     const SearchSpace& eff = effective(t);
+    ktc::trace_phase("tune: + effective space", tb);
     std::vector<Backend*> bes;
     for (auto& b : t->backends) bes.push_back(b.get());
     for (Backend* b : bes)
@@ -517,6 +521,7 @@ void tune(ktc_tuner* t) {
     std::unique_ptr<ResultLog> log;
     if (!t->checkpoint.empty()) log = std::make_unique<ResultLog>(t->checkpoint);
     TuningOutcome o = run_tuning_sharded(t->job, bes, eff, t->subset, log.get());
+    ktc::trace_phase("tune: + search", tb);
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     ktc_summary& s = t->summary;
     std::memset(&s, 0, sizeof(s));
@@ -598,7 +603,11 @@ int ktc_tuner_create(ktc_tuner** out) {
     return KTC_OK;
 }
 
-void ktc_tuner_destroy(ktc_tuner* t) { delete t; }
+void ktc_tuner_destroy(ktc_tuner* t) {
+    const auto t0 = std::chrono::steady_clock::now();
+    delete t;
+    ktc::trace_phase("tuner destroy", t0);
+}
 
 int ktc_tuner_template_conv(ktc_tuner* t, size_t x, size_t y, int filter, float weight,
                             uint64_t seed) {

@@ -257,29 +257,6 @@ void CompileService::run_batch(Batch b) {
         for (Item* it : all) compile_group({it});  // attribute errors to their configuration
 }
 
-// Work-conserving batching: a batch taken while other pool threads sit idle
-// (and no other batch is waiting for them) is split so they share it.  Full
-// batches amortize NVRTC's fixed cost when the pool is saturated; on a burst
-// into an idle pool (a fresh job, the head of a search) smaller programs
-// finish sooner, and the first configurations -- kept by this thread --
-// are the ones the evaluator needs first.
-void CompileService::split_for_idle_locked(Batch& b) {
-    if (!b.src || !b.src->batchable || b.items.size() < 2) return;
-    const size_t spare = size_t(idle_) > ready_.size() ? size_t(idle_) - ready_.size() : 0;
-    if (spare == 0) return;
-    const size_t parts = std::min(spare + 1, b.items.size());
-    const size_t keep = (b.items.size() + parts - 1) / parts;
-    Batch rest;
-    rest.src = b.src;
-    rest.problem = b.problem;
-    rest.born = b.born;
-    rest.items.assign(std::make_move_iterator(b.items.begin() + keep),
-                      std::make_move_iterator(b.items.end()));
-    b.items.resize(keep);
-    ready_.push_front(std::move(rest));
-    cv_.notify_one();
-}
-
 int CompileService::threads() {
     std::lock_guard<std::mutex> lk(mu_);
     return want_threads_ > 0 ? want_threads_ : int(std::max(1u, std::thread::hardware_concurrency()));
@@ -290,43 +267,81 @@ int CompileService::batch() {
     return batch_;
 }
 
+// Program formation (under mu_).  Configurations wait as items in one queue
+// per (source, problem); a thread that picks work forms its NVRTC program
+// then, from the queue of the oldest item:
+//   * the most expensive queued item first (longest-processing-time-first:
+//     the makespan of a burst -- a fresh job, the end of a search -- is set
+//     by its slowest compile, so that one must not start last);
+//   * then further items, cheapest first, while the program stays within
+//     this thread's fair share of the queued cost (total / pool threads)
+//     and `batch_` items.
+// A backlogged pool therefore builds full programs (NVRTC's fixed ~50 ms per
+// program amortized); an under-loaded one spreads the work evenly.  Items
+// the evaluator needs before a pool thread took them are compiled by the
+// evaluator itself (get()), so nothing waits behind the ordering.
+bool CompileService::take_program_locked(Batch* out) {
+    auto qit = queues_.end();
+    for (auto it = queues_.begin(); it != queues_.end(); ++it)
+        if (!it->second.items.empty() &&
+            (qit == queues_.end() || it->second.oldest() < qit->second.oldest()))
+            qit = it;
+    if (qit == queues_.end()) return false;
+    Queue& q = qit->second;
+    out->src = q.src;
+    out->problem = q.problem;
+    out->items.clear();
+    auto take = [&](size_t i) {
+        queued_cost_ -= q.items[i].cost;
+        out->items.push_back(std::move(q.items[i]));
+        q.items.erase(q.items.begin() + long(i));
+    };
+    if (!q.src->batchable) {
+        size_t oldest = 0;
+        for (size_t i = 1; i < q.items.size(); ++i)
+            if (q.items[i].born < q.items[oldest].born) oldest = i;
+        take(oldest);
+    } else {
+        size_t big = 0;
+        for (size_t i = 1; i < q.items.size(); ++i)
+            if (q.items[i].cost > q.items[big].cost) big = i;
+        double total = q.items[big].cost;
+        const double share = (queued_cost_ + total_inflight_) / double(std::max(1, want_threads_));
+        take(big);
+        while (!q.items.empty() && int(out->items.size()) < batch_) {
+            size_t small = 0;
+            for (size_t i = 1; i < q.items.size(); ++i)
+                if (q.items[i].cost < q.items[small].cost) small = i;
+            if (total + q.items[small].cost > share) break;
+            total += q.items[small].cost;
+            take(small);
+        }
+    }
+    if (q.items.empty()) queues_.erase(qit);
+    return true;
+}
+
 void CompileService::worker() {
-    using namespace std::chrono;
     for (;;) {
         Batch b;
+        double cost = 0.0;
         {
             std::unique_lock<std::mutex> lk(mu_);
-            for (;;) {
-                if (!ready_.empty()) {
-                    b = std::move(ready_.front());
-                    ready_.pop_front();
-                    split_for_idle_locked(b);
-                    break;
-                }
-                // A partially filled batch is taken once it has waited a
-                // little for company (prefetch bursts fill batches quickly).
-                auto oldest = pending_.end();
-                for (auto it = pending_.begin(); it != pending_.end(); ++it)
-                    if (oldest == pending_.end() || it->second.born < oldest->second.born) oldest = it;
-                if (oldest != pending_.end() &&
-                    steady_clock::now() - oldest->second.born > milliseconds(10)) {
-                    b = std::move(oldest->second);
-                    pending_.erase(oldest);
-                    split_for_idle_locked(b);
-                    break;
-                }
-                ++idle_;
-                cv_.wait_for(lk, milliseconds(oldest == pending_.end() ? 100 : 3));
-                --idle_;
-            }
+            cv_.wait(lk, [&] { return !queues_.empty(); });
+            take_program_locked(&b);
+            for (const Item& it : b.items) cost += it.cost;
+            total_inflight_ += cost;
         }
         run_batch(std::move(b));
+        std::lock_guard<std::mutex> lk(mu_);
+        total_inflight_ -= cost;
     }
 }
 
 std::shared_future<KernelPtr> CompileService::enlist_locked(const KernelSource& src,
                                                             const Defines& problem,
-                                                            const Defines& config, bool* created) {
+                                                            const Defines& config, double cost,
+                                                            bool* created) {
     const std::string key = key_of(src, problem, config);
     auto it = cache_.find(key);
     if (it != cache_.end()) {
@@ -338,35 +353,31 @@ std::shared_future<KernelPtr> CompileService::enlist_locked(const KernelSource& 
     std::shared_future<KernelPtr> fut = promise->get_future().share();
     if (cache_.size() > 50000) cache_.clear();  // bound host memory
     cache_.emplace(key, fut);
-    const std::string bkey = src.batchable ? batch_key_of(src, problem) : key;
+    const std::string qkey = src.batchable ? batch_key_of(src, problem) : key;
     auto& sp = sources_[src.id];
     if (!sp) sp = std::make_shared<const KernelSource>(src);
-    Batch& b = pending_[bkey];
-    if (b.items.empty()) {
-        b.src = sp;
-        b.problem = problem;
-        b.born = std::chrono::steady_clock::now();
+    Queue& q = queues_[qkey];
+    if (!q.src) {
+        q.src = sp;
+        q.problem = problem;
     }
-    b.items.push_back(Item{config, key, promise});
-    if (int(b.items.size()) >= batch_ || !src.batchable) {
-        ready_.push_back(std::move(b));
-        pending_.erase(bkey);
-        cv_.notify_one();
-    }
+    q.items.push_back(Item{config, key, promise, std::max(cost, 1e-3),
+                           std::chrono::steady_clock::now()});
+    queued_cost_ += q.items.back().cost;
+    cv_.notify_one();
     return fut;
 }
 
 void CompileService::prefetch(const KernelSource& src, const Defines& problem,
-                              const Defines& config) {
+                              const Defines& config, double cost) {
     std::lock_guard<std::mutex> lk(mu_);
     ensure_workers_locked();
     bool created = false;
-    enlist_locked(src, problem, config, &created);
-    cv_.notify_one();
+    enlist_locked(src, problem, config, cost, &created);
 }
 
 KernelPtr CompileService::get(const KernelSource& src, const Defines& problem,
-                              const Defines& config, bool* hit) {
+                              const Defines& config, bool* hit, double cost) {
     std::shared_future<KernelPtr> fut;
     Batch mine;
     bool run_here = false;
@@ -374,18 +385,23 @@ KernelPtr CompileService::get(const KernelSource& src, const Defines& problem,
         std::lock_guard<std::mutex> lk(mu_);
         ensure_workers_locked();
         bool created = false;
-        fut = enlist_locked(src, problem, config, &created);
+        fut = enlist_locked(src, problem, config, cost, &created);
         if (hit) *hit = !created && fut.wait_for(std::chrono::seconds(0)) == std::future_status::ready;
-        // Still waiting in a filling batch: compile that batch right here.
-        const std::string bkey =
-            src.batchable ? batch_key_of(src, problem) : key_of(src, problem, config);
-        auto pit = pending_.find(bkey);
-        if (pit != pending_.end()) {
-            const std::string key = key_of(src, problem, config);
-            for (const Item& it : pit->second.items)
-                if (it.key == key) {
-                    mine = std::move(pit->second);
-                    pending_.erase(pit);
+        // Still queued (no pool thread took it yet): compile it right here,
+        // alone -- the caller is waiting for exactly this configuration.
+        const std::string key = key_of(src, problem, config);
+        const std::string qkey = src.batchable ? batch_key_of(src, problem) : key;
+        auto qit = queues_.find(qkey);
+        if (qit != queues_.end()) {
+            Queue& q = qit->second;
+            for (size_t i = 0; i < q.items.size(); ++i)
+                if (q.items[i].key == key) {
+                    mine.src = q.src;
+                    mine.problem = q.problem;
+                    queued_cost_ -= q.items[i].cost;
+                    mine.items.push_back(std::move(q.items[i]));
+                    q.items.erase(q.items.begin() + long(i));
+                    if (q.items.empty()) queues_.erase(qit);
                     run_here = true;
                     break;
                 }

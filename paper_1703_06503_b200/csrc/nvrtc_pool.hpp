@@ -78,10 +78,12 @@ class CompileService {
     // configurations per NVRTC program (1 disables batching).
     void configure(int threads, const std::string& cache_dir, int batch = 8);
 
+    // `cost`: relative compile-cost estimate (1 ~ a small configuration),
+    // used to order and size programs (see take_program_locked).
     KernelPtr get(const KernelSource& src, const Defines& problem, const Defines& config,
-                  bool* hit);
-    void prefetch(const KernelSource& src, const Defines& problem, const Defines& config);
-
+                  bool* hit, double cost = 1.0);
+    void prefetch(const KernelSource& src, const Defines& problem, const Defines& config,
+                  double cost = 1.0);
     int threads();
     int batch();
     double total_compile_ms();
@@ -94,36 +96,47 @@ class CompileService {
         Defines config;
         std::string key;
         std::shared_ptr<std::promise<KernelPtr>> promise;
+        double cost = 1.0;
+        std::chrono::steady_clock::time_point born;
     };
-    struct Batch {
+    struct Batch {  // one NVRTC program
         std::shared_ptr<const KernelSource> src;
         Defines problem;
         std::vector<Item> items;
-        std::chrono::steady_clock::time_point born;
+    };
+    struct Queue {  // waiting configurations of one (source, problem)
+        std::shared_ptr<const KernelSource> src;
+        Defines problem;
+        std::vector<Item> items;
+        std::chrono::steady_clock::time_point oldest() const {
+            auto t = items.front().born;
+            for (const Item& it : items) t = std::min(t, it.born);
+            return t;
+        }
     };
     std::string key_of(const KernelSource& src, const Defines& problem, const Defines& config) const;
     std::string batch_key_of(const KernelSource& src, const Defines& problem) const;
     void run_batch(Batch b);
-    void split_for_idle_locked(Batch& b);
+    bool take_program_locked(Batch* out);
     void worker();
     void ensure_workers_locked();
-    // Registers `config` (if new) in the pending batch of its key; returns
-    // the future and whether this call created it.
+    // Registers `config` (if new) in its queue; returns the future and
+    // whether this call created it.
     std::shared_future<KernelPtr> enlist_locked(const KernelSource& src, const Defines& problem,
-                                                const Defines& config, bool* created);
+                                                const Defines& config, double cost, bool* created);
     KernelPtr load_disk(const std::string& key);
     void store_disk(const std::string& key, const CompiledKernel& k);
 
     std::mutex mu_;
     std::condition_variable cv_;
-    std::deque<Batch> ready_;                         // full batches
-    std::map<std::string, Batch> pending_;            // filling batches by batch key
+    std::map<std::string, Queue> queues_;  // by batch key (source, problem)
+    double queued_cost_ = 0.0;               // sum of queued item costs
+    double total_inflight_ = 0.0;            // cost of programs being compiled
     std::unordered_map<std::string, std::shared_future<KernelPtr>> cache_;
     std::map<std::string, std::shared_ptr<const KernelSource>> sources_;
     std::vector<std::thread> workers_;
     int want_threads_ = 0;
     int batch_ = 8;
-    int idle_ = 0;  // pool threads waiting for work
     std::string cache_dir_;
     double compile_ms_ = 0.0;
     size_t programs_ = 0;
