@@ -179,6 +179,104 @@ __device__ __forceinline__ void vp_f32(VerifyPartial& p, unsigned long long i, f
     }
 }
 
+// fp32 screen in front of vp_f32: an element whose effect on the state is
+// provably nil is skipped without any double arithmetic.  With D = |c - r|
+// (exact) and the float estimate df = fl(|c - r|) (relative error <= 2^-24):
+//   * pass is certain when df <= 0.5 * fl(rel * |r| + abs)  (margin >> float
+//     rounding of the tolerance), so first_fail cannot move;
+//   * D > max_abs is impossible when df < abs_lo = rd(max_abs * (1 - 2^-20));
+//   * D / |r| > max_rel is impossible when df < fl(rel_lo * |r|), rel_lo =
+//     rd(max_rel * (1 - 2^-20));
+//   * non-finite inputs, |r| == 0 while max_rel < 0, and everything else take
+//     the exact double path, which then refreshes the screen thresholds.
+// The screened rule is therefore identical to vp_f32 (same state, bit for
+// bit); it only moves the common case -- a passing element below both running
+// maxima -- onto a handful of FP32 instructions, so the verifier runs at the
+// HBM rate of its two input streams instead of the FP64 rate.
+// Ties matter: outputs of a passing kernel differ from the reference by a
+// few ulps, so many elements share the running maximum exactly.  When c and
+// r are within a factor of two of each other (same sign), c - r is exact in
+// float (Sterbenz), df == D, and "D <= rd(max_abs)" settles the strict
+// comparison without the margin.
+struct VerifyScreen {
+    float abs_rd;   // rd(max_abs)
+    float abs_lo;   // rd(max_abs * (1 - 2^-20))
+    float rel_lo;   // rd(max_rel * (1 - 2^-20))
+    bool rel_nonneg;  // max_rel >= 0 (a zero relative error cannot raise it)
+};
+
+// Pins a value in a register: without it ptxas rematerializes the
+// thresholds from the double state (F2F + DSETP) at every use in the hot loop.
+__device__ __forceinline__ float pin(float v) {
+    asm volatile("mov.b32 %0, %0;" : "+f"(v));
+    return v;
+}
+
+__device__ __forceinline__ void vs_refresh(VerifyScreen& s, const VerifyPartial& p) {
+    s.abs_rd = pin(__double2float_rd(p.max_abs));
+    s.abs_lo = pin(__double2float_rd(p.max_abs * (1.0 - 0x1.0p-20)));
+    s.rel_lo = pin(__double2float_rd(p.max_rel * (1.0 - 0x1.0p-20)));
+    s.rel_nonneg = pin(p.max_rel >= 0.0 ? 1.0f : 0.0f) != 0.0f;
+}
+
+// Thresholds shared by the warp.  The report keeps the maximum over ALL
+// elements (lowest index on ties), so an element strictly below an error
+// some other lane has already seen can never be the final maximum, whatever
+// this lane's own running state says; per-lane records alone would flag
+// ~ln(n)/n of the elements, and a flag costs the whole (divergent) warp.
+struct WarpScreen {
+    float abs_rd;  // rd(max over lanes of max_abs): an attained error
+    float abs_lo;  // the same with the 2^-20 margin for inexact differences
+    float rel_lo;  // rd(max over lanes of max_rel * (1 - 2^-20))
+};
+
+__device__ __forceinline__ void ws_refresh(WarpScreen& w, const VerifyScreen& s) {
+    float a = s.abs_rd, l = s.abs_lo, r = s.rel_lo;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+        l = fmaxf(l, __shfl_xor_sync(0xffffffffu, l, o));
+        r = fmaxf(r, __shfl_xor_sync(0xffffffffu, r, o));
+    }
+    w.abs_rd = a;
+    w.abs_lo = l;
+    w.rel_lo = r;
+}
+
+// Per-batch screen thresholds (lane state merged with the warp's).
+struct ScreenThr {
+    float abs_le;  // skip an exact difference D <= abs_le
+    float rel_lt;  // skip when D < rel_lt * |r|
+    bool zero_ok;  // a zero error cannot raise max_rel
+};
+
+__device__ __forceinline__ ScreenThr screen_thresholds(const VerifyScreen& s, const WarpScreen& w) {
+    ScreenThr t;
+    // Own maximum: ties keep the earlier index, so D == max_abs is a no-op.
+    // Another lane's maximum only dominates strictly: one float below it.
+    t.abs_le = pin(fmaxf(s.abs_rd, nextafterf(w.abs_rd, -INFINITY)));
+    t.rel_lt = pin(fmaxf(s.rel_lo, w.rel_lo));
+    t.zero_ok = s.rel_nonneg;
+    return t;
+}
+
+// True when element i might change the state (then vp_f32 decides exactly).
+// `close` (|c - r| <= 2^-10 |r|) puts c and r within a factor of two of each
+// other with the same sign, so fl(c - r) is exact (Sterbenz) and df == D;
+// anything else -- far apart, zero reference with nonzero candidate,
+// non-finite -- is flagged.
+__device__ __forceinline__ bool vs_needs(const ScreenThr& t, float cf, float rf, float half_rel,
+                                         float half_abs) {
+    const float df = fabsf(cf - rf);
+    const float mf = fabsf(rf);
+    const bool ok = df <= fmaf(half_rel, mf, half_abs)   // certain pass (NaN compares false)
+                    && df <= mf * 0x1.0p-10f              // close: exact difference
+                    && df <= t.abs_le                     // cannot raise max_abs
+                    && (df < t.rel_lt * mf || (df == 0.0f && t.zero_ok))  // nor max_rel
+                    && mf <= 3.4028234663852886e38f;      // finite
+    return !ok;
+}
+
 __device__ __forceinline__ void vp_i32(VerifyPartial& p, unsigned long long i, int ci, int ri) {
     const double abs_err = fabs((double)ci - (double)ri);
     if (ci != ri && i < p.first_fail) p.first_fail = i;
@@ -205,26 +303,72 @@ ktc_verify_partial(const void* __restrict__ cand, const void* __restrict__ ref,
         const float* c = (const float*)cand;
         const float* r = (const float*)ref;
         const unsigned long long end4 = begin + ((end > begin ? end - begin : 0) & ~3ull);
-        // Four independent partial states (one per float4 lane) break the
-        // running-max dependency chain; each lane's indices still increase,
-        // and vp_merge is the same exact rule used across threads.
-        VerifyPartial q1, q2, q3;
-        vp_init(q1);
-        vp_init(q2);
-        vp_init(q3);
-#pragma unroll 2
-        for (unsigned long long i = begin + 4ull * threadIdx.x; i < end4;
-             i += 4ull * KTC_VERIFY_THREADS) {
-            const float4 cv = __ldg(reinterpret_cast<const float4*>(c + i));
-            const float4 rv = __ldg(reinterpret_cast<const float4*>(r + i));
-            vp_f32(p, i, cv.x, rv.x, rel_tol, abs_tol);
-            vp_f32(q1, i + 1, cv.y, rv.y, rel_tol, abs_tol);
-            vp_f32(q2, i + 2, cv.z, rv.z, rel_tol, abs_tol);
-            vp_f32(q3, i + 3, cv.w, rv.w, rel_tol, abs_tol);
+        // One state per thread: the fp32 screen settles almost every element
+        // without touching the running maxima, so there is no dependency
+        // chain to break.  U float4 pairs are loaded before any is screened
+        // (memory-level parallelism for the two HBM streams); flagged
+        // elements then go through the exact rule in index order, in one
+        // rolled loop (one copy of the double-precision code).  Skips stay valid while flagged elements update the state:
+        // the maxima only grow and first_fail only shrinks.
+        VerifyScreen sc;
+        vs_refresh(sc, p);
+        WarpScreen ws;
+        ws_refresh(ws, sc);
+        // Tolerances beyond float range would make the fp32 pass screen
+        // unsound; then every element is flagged (exact path).
+        const bool tol_ok = rel_tol < 1e30 && abs_tol < 1e30;
+        const float half_rel = tol_ok ? 0.5f * (float)rel_tol : -INFINITY;
+        const float half_abs = tol_ok ? 0.5f * (float)abs_tol : -INFINITY;
+        constexpr int U = 4;
+        const unsigned long long step = 4ull * KTC_VERIFY_THREADS;
+        // Warp-uniform trip count (the warp's first lane drives the loop),
+        // so the warp-wide threshold exchange below never diverges.
+        const unsigned long long lane4 = 4ull * (threadIdx.x & 31);
+        for (unsigned long long w0 = begin + 4ull * (threadIdx.x & ~31u); w0 < end4; w0 += U * step) {
+            const unsigned long long i0 = w0 + lane4;
+            float4 cv[U], rv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const unsigned long long i = i0 + u * step;
+                if (i < end4) {
+                    cv[u] = __ldcs(reinterpret_cast<const float4*>(c + i));
+                    rv[u] = __ldg(reinterpret_cast<const float4*>(r + i));
+                } else {
+                    cv[u] = rv[u] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                }
+            }
+            const ScreenThr thr = screen_thresholds(sc, ws);
+            unsigned need = 0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                need |= unsigned(vs_needs(thr, cv[u].x, rv[u].x, half_rel, half_abs)) << (4 * u);
+                need |= unsigned(vs_needs(thr, cv[u].y, rv[u].y, half_rel, half_abs)) << (4 * u + 1);
+                need |= unsigned(vs_needs(thr, cv[u].z, rv[u].z, half_rel, half_abs)) << (4 * u + 2);
+                need |= unsigned(vs_needs(thr, cv[u].w, rv[u].w, half_rel, half_abs)) << (4 * u + 3);
+                if (i0 + u * step >= end4) need &= ~(0xfu << (4 * u));
+            }
+#pragma unroll 1
+            while (need) {
+                const int b = __ffs(need) - 1;
+                need &= need - 1;
+                const unsigned long long i = i0 + (b >> 2) * step + (b & 3);
+                // The pair from registers (a select chain, no dynamic
+                // indexing): re-reading memory here would put a round trip
+                // on every flagged element of every lane.
+                float cf = 0.0f, rf = 0.0f;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if ((b >> 2) == u) {
+                        const int l = b & 3;
+                        cf = l == 0 ? cv[u].x : l == 1 ? cv[u].y : l == 2 ? cv[u].z : cv[u].w;
+                        rf = l == 0 ? rv[u].x : l == 1 ? rv[u].y : l == 2 ? rv[u].z : rv[u].w;
+                    }
+                }
+                vp_f32(p, i, cf, rf, rel_tol, abs_tol);
+                vs_refresh(sc, p);
+            }
+            ws_refresh(ws, sc);  // every lane reaches here: the loop bound is warp-uniform
         }
-        vp_merge(p, q1);
-        vp_merge(p, q2);
-        vp_merge(p, q3);
         for (unsigned long long i = end4 + threadIdx.x; i < end; i += KTC_VERIFY_THREADS)
             vp_f32(p, i, __ldg(c + i), __ldg(r + i), rel_tol, abs_tol);
     } else {

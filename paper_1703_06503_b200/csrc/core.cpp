@@ -276,7 +276,14 @@ static int setup_ctx(ktc_ctx* c) {
         if (rc != CUDA_SUCCESS) return fail_cu(c, rc, f.name);
     }
     query_limits(c);
-    c->verify_blocks = std::max(1, c->limits.sm_count * 4);
+    // One full wave of verifier blocks (a partial second wave would run the
+    // tail of both HBM streams at a fraction of the bandwidth).
+    int per_sm = 0;
+    if (d.cuOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->fn_verify_partial, 256, 0) !=
+            CUDA_SUCCESS ||
+        per_sm < 1)
+        per_sm = 2;
+    c->verify_blocks = std::max(1, c->limits.sm_count * per_sm);
     size_t scratch = 256 + sizeof(KtcVerifyPartial) * size_t(c->verify_blocks);
     rc = d.cuMemAlloc(&c->scratch, scratch);
     if (rc != CUDA_SUCCESS) return fail_cu(c, rc, "cuMemAlloc(scratch)");

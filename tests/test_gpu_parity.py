@@ -191,6 +191,50 @@ def test_device_verifier_matches_host_rule(backend):
             assert (np.isnan(a) and np.isnan(b)) or a == b, (key, got, want)
 
 
+def _screen_cases():
+    """Adversarial cases for the verifier's fp32 screen: errors straddling the
+    tolerance, records set late, ties, denormal / zero references, and
+    tolerances at the edges of float range."""
+    rng = np.random.default_rng(11)
+    n = 2_000_003
+    ref = (rng.random(n, dtype=np.float32) * 2 - 1) * np.float32(3.0)
+    ref[::97] = 0.0
+    ref[5::101] = np.float32(1e-40)  # denormal references
+    out = []
+    # relative errors spread across the 1e-4 threshold (some pass, some fail)
+    e = rng.uniform(-2e-4, 2e-4, n).astype(np.float32)
+    out.append(((ref * (1 + e)).astype(np.float32), ref, 1e-4, 1e-6))
+    # exactly at / around the tolerance boundary, all in the same buffer
+    c = ref.copy()
+    idx = rng.choice(n, 5000, replace=False)
+    t = (1e-6 + 1e-4 * np.abs(ref[idx].astype(np.float64)))
+    c[idx] = (ref[idx].astype(np.float64) + t * rng.choice([0.999999, 1.0, 1.000001], 5000)).astype(np.float32)
+    out.append((c, ref, 1e-4, 1e-6))
+    # a monotonically growing error (a new record on every element)
+    g = ref + np.linspace(0, 1e-3, n, dtype=np.float32)
+    out.append((g.astype(np.float32), ref, 1e-4, 1e-6))
+    # many exact ties of the maximum error
+    tie = ref.copy()
+    tie[rng.choice(n, 1000, replace=False)] += np.float32(0.5)
+    out.append((tie, ref, 1e-4, 1e-6))
+    # zero tolerances, and tolerances beyond float range
+    out.append(((ref * (1 + e)).astype(np.float32), ref, 0.0, 0.0))
+    out.append(((ref * (1 + e)).astype(np.float32), ref, 1e40, 1e-6))
+    out.append(((ref * (1 + e)).astype(np.float32), ref, 1e-4, 1e40))
+    return out
+
+
+def test_device_verifier_screen_is_exact(backend):
+    for cand, ref, rel, abs_ in _screen_cases():
+        want = O.verify(cand, ref, rel, abs_)
+        got = backend.verify_pair(cand, ref, rel, abs_)
+        for key in ("pass", "buffer_index", "element_index", "elements_compared"):
+            assert got[key] == want[key], (key, rel, abs_, got, want)
+        for key in ("max_abs_error", "max_rel_error"):
+            a, b = got[key], want[key]
+            assert (np.isnan(a) and np.isnan(b)) or a == b, (key, rel, abs_, got, want)
+
+
 def test_device_verifier_i32(backend):
     ref = np.arange(5000, dtype=np.int32)
     cand = ref.copy(); cand[1234] += 2
