@@ -228,6 +228,14 @@ typedef struct {
     int compile_threads;    /* NVRTC pool size; 0 = hardware threads */
     const char* cache_dir;  /* on-disk cubin cache; NULL = memory only */
     int digest_outputs;     /* also FNV-digest outputs (D2H + host hash); default 0 */
+    /* Early-out for device-bound searches; 0 (default) = off.  When > 0 and
+     * the first flushed timed launch of a configuration takes more than
+     * prune_factor x the best verified time this backend has seen for the
+     * same argument list, the remaining repetitions are skipped and that
+     * launch is the row's time (it is still verified).  Such a
+     * configuration cannot become the best unless its best-of-N time is
+     * below 1/prune_factor of its first flushed launch. */
+    double prune_factor;
 } ktc_backend_options;
 
 void ktc_backend_default_options(ktc_backend_options* opts);

@@ -96,7 +96,7 @@ class BackendOptions(C.Structure):
     _fields_ = [
         ("warmup", C.c_int), ("flush_l2", C.c_int), ("verify", C.c_int), ("rel_tol", C.c_double),
         ("abs_tol", C.c_double), ("compile_threads", C.c_int), ("cache_dir", C.c_char_p),
-        ("digest_outputs", C.c_int),
+        ("digest_outputs", C.c_int), ("prune_factor", C.c_double),
     ]
 
 

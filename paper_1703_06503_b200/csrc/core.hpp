@@ -62,6 +62,12 @@ const std::string& last_error();
 bool trace_on();
 void trace_phase(const char* what, std::chrono::steady_clock::time_point since);
 
+// ktc_launch_timed with the prune_factor early-out (see ktc.h).
+extern "C" int ktc_launch_timed_pruned(ktc_ctx* ctx, ktc_fn* fn, const unsigned grid[3],
+                                       const unsigned block[3], unsigned smem_bytes, void** params,
+                                       int warmup, int reps, int flush, double bar,
+                                       float* best_ms, float* all_ms, int* reps_done);
+
 // Bumped whenever a primary context is reset (destroyed): host allocations
 // tied to the old context (pinned recipe copies) are gone with it.
 unsigned primary_ctx_epoch();

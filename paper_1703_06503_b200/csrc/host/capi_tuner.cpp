@@ -487,7 +487,7 @@ void ensure_backends(ktc_tuner* t) {
     for (int d : t->devices) key += ":" + std::to_string(d);
     key += "|" + std::to_string(t->opts.flush_l2) + std::to_string(t->opts.warmup) +
            std::to_string(t->opts.compile_threads) + std::to_string(t->job.rel_tol) +
-           std::to_string(t->job.abs_tol);
+           std::to_string(t->job.abs_tol) + "|" + std::to_string(t->opts.prune_factor);
     if (key == t->backends_key && !t->backends.empty()) return;
     t->backends.clear();
     if (t->backend_spec == "cuda") {

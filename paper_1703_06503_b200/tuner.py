@@ -179,6 +179,14 @@ class Tuner:
     def SetVerification(self, verify: bool = True, rel_tol: float = 1e-4, abs_tol: float = 1e-6):
         K.check(self._lib.ktc_tuner_set_verification(self._h, int(verify), rel_tol, abs_tol))
 
+    def SetPruning(self, factor: float):
+        """Early-out for device-bound searches (ktc.h prune_factor; 0 = off): a
+        configuration whose first flushed launch exceeds `factor` x the best
+        verified time seen so far is timed once instead of best-of-N."""
+        self._opts.prune_factor = float(factor)
+        K.check(self._lib.ktc_tuner_set_backend(self._h, self._backend.encode(),
+                                                C.byref(self._opts)))
+
     def SetSubset(self, indices: Sequence[int]):
         arr, n = _arr(C.c_uint64, indices)
         K.check(self._lib.ktc_tuner_set_subset(self._h, arr, n))

@@ -278,3 +278,28 @@ def test_gemm_tf32_tcgen05_configs(backend, m, n, k):
                 assert rep["pass"], (cfg, rep)
                 seen += 1
     assert seen >= 6
+
+
+def test_prune_factor_early_out_keeps_winner_and_verification(built):
+    """prune_factor (ktc.h): slow configurations are timed once, still verified;
+    the winner's time is unaffected (it is never pruned: its first launch is
+    within the factor of the best seen)."""
+    def run(prune):
+        t = pkg.Tuner.gemm(1024, 1024, 1024, devices=[0])
+        t.UseRandomSearch(1 / 4096)
+        t.SetVerification(True)
+        t.SetRepetitions(3)
+        if prune:
+            t.SetPruning(prune)
+        s = t.Tune()
+        return t, s
+
+    full, s_full = run(0.0)
+    pruned, s_pruned = run(1.5)
+    rows_f, rows_p = full.rows(), pruned.rows()
+    assert [r.config for r in rows_f] == [r.config for r in rows_p]
+    assert all(r.verified == "pass" for r in rows_p if r.status == "ok")
+    assert s_pruned["kernel_launches"] < s_full["kernel_launches"]
+    _, best_f = full.GetBestResult()
+    _, best_p = pruned.GetBestResult()
+    assert abs(best_p - best_f) / best_f < 0.05, (best_f, best_p)

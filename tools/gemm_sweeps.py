@@ -52,8 +52,10 @@ def shape_sweep(fraction: float, out: dict, strategies=("annealing", "pso")):
             print(json.dumps(rec), flush=True)
 
 
-def throughput_4096(sample: int, out: dict):
+def throughput_4096(sample: int, out: dict, prune: float = 0.0):
     t = pkg.Tuner.gemm(4096, 4096, 4096)
+    if prune:
+        t.SetPruning(prune)
     _, _, valid = t.space_counts()
     idx = sorted(random.Random(1).sample(range(valid), sample))
     t.SetVerification(True)
@@ -66,8 +68,8 @@ def throughput_4096(sample: int, out: dict):
     rec = {"m": 4096, "sample": sample, "space": valid, "wall_s": wall,
            "configs_per_s": sample / wall, "best_config": cfg, "best_ms": ms,
            "gflops": 2.0 * 4096 ** 3 / ms / 1e6, "failed": s["failed_evaluations"],
-           "compile_s": s["compile_s"], "device_s": s["device_s"]}
-    out["throughput_4096"] = rec
+           "compile_s": s["compile_s"], "device_s": s["device_s"], "prune_factor": prune}
+    out["throughput_4096" + (f"_prune{prune:g}" if prune else "")] = rec
     print(json.dumps(rec), flush=True)
 
 
@@ -77,10 +79,14 @@ def main():
     ap.add_argument("--sample", type=int, default=1024)
     ap.add_argument("--skip-shapes", action="store_true")
     ap.add_argument("--skip-4096", action="store_true")
+    ap.add_argument("--prune", type=float, default=0.0,
+                    help="also measure the 4096 sample with this prune_factor")
     args = ap.parse_args()
     out = {}
     if not args.skip_4096:
         throughput_4096(args.sample, out)
+        if args.prune:
+            throughput_4096(args.sample, out, args.prune)
     if not args.skip_shapes:
         shape_sweep(args.fraction, out)
     p = ROOT / "gpurun_out" / "gemm_sweeps.json"
