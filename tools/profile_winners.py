@@ -32,6 +32,10 @@ def main():
             _, size, cfg = w.split(":", 2)
             m = int(size)
             r = be.evaluate(pkg.gemm_request(m, m, m, pkg.parse_canonical(cfg), reps=2))
+        elif w.startswith("tf32:"):  # tf32:<size>:<canonical config>
+            _, size, cfg = w.split(":", 2)
+            m = int(size)
+            r = be.evaluate(pkg.gemm_request(m, m, m, pkg.parse_canonical(cfg), reps=2, tf32=True))
         elif w == "gemm":
             cfg = table["gemm"]["2048"]["config"]
             r = be.evaluate(pkg.gemm_request(2048, 2048, 2048, pkg.parse_canonical(cfg), reps=2))
