@@ -306,6 +306,17 @@ int ktc_tuner_add_constraint(ktc_tuner* t, const char* expr);
 int ktc_tuner_add_modifier(ktc_tuner* t, int target, int op, const char* const* factors, int n);
 int ktc_tuner_set_local_memory(ktc_tuner* t, const char* expr);
 int ktc_tuner_add_argument(ktc_tuner* t, const ktc_arg* arg);
+/* CLTune SetReference(files, name, global, local): a reference kernel (no
+ * tuning parameters) run once on the device over the job's arguments at the
+ * start of Tune(); its outputs become the reference every configuration is
+ * verified against (on the device).  Replaces ktune's TuningJob::reference
+ * callback (tuner.hpp:147) for custom kernels. */
+int ktc_tuner_set_reference_kernel(ktc_tuner* t, const char* source_ref, const char* name,
+                                   int ndim, const size_t* global, const size_t* local);
+/* The same with host reference outputs (one buffer per output argument, in
+ * order; types KTC_F32 / KTC_I32), copied. */
+int ktc_tuner_set_reference_outputs(ktc_tuner* t, int n, const void* const* buffers,
+                                    const size_t* lengths, const int* types);
 int ktc_tuner_set_device(ktc_tuner* t, const ktc_device_model* dev);
 int ktc_tuner_set_strategy(ktc_tuner* t, int kind, double fraction, double temperature,
                            double alpha, double beta, double gamma, size_t swarm);

@@ -196,6 +196,10 @@ _SIGS = {
     "ktc_tuner_add_modifier": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_char_p), C.c_int]),
     "ktc_tuner_set_local_memory": (C.c_int, [_P, C.c_char_p]),
     "ktc_tuner_add_argument": (C.c_int, [_P, C.POINTER(Arg)]),
+    "ktc_tuner_set_reference_kernel": (C.c_int, [_P, C.c_char_p, C.c_char_p, C.c_int,
+                                                 C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+    "ktc_tuner_set_reference_outputs": (C.c_int, [_P, C.c_int, C.POINTER(C.c_void_p),
+                                                  C.POINTER(C.c_size_t), C.POINTER(C.c_int)]),
     "ktc_tuner_set_device": (C.c_int, [_P, C.POINTER(DeviceModel)]),
     "ktc_tuner_set_strategy": (C.c_int, [_P, C.c_int, C.c_double, C.c_double, C.c_double,
                                          C.c_double, C.c_double, C.c_size_t]),

@@ -36,6 +36,14 @@ struct ktc_tuner {
     std::string backends_key;
     std::optional<TuningOutcome> outcome;
     ktc_summary summary{};
+    // CLTune SetReference: a reference kernel run once on the device over
+    // the same arguments; its outputs become the verification reference.
+    struct RefKernel {
+        std::string source_ref, name;
+        std::vector<size_t> global, local;
+    };
+    std::optional<RefKernel> ref_kernel;
+    std::optional<std::vector<Buffer>> ref_outputs;  // computed or user-given
 };
 
 namespace {
@@ -507,10 +515,50 @@ void ensure_backends(ktc_tuner* t) {
     t->backends_key = key;
 }
 
+// Runs the CLTune reference kernel once (first device) over the job's
+// arguments and keeps its outputs as the host reference of the job.
+void compute_reference_outputs(ktc_tuner* t) {
+    auto* cb = t->backends.empty() ? nullptr : dynamic_cast<CudaBackend*>(t->backends[0].get());
+    if (!cb) throw Error("SetReference(kernel) needs the cuda backend");
+    const auto& rk = *t->ref_kernel;
+    EvaluationRequest req;
+    req.kernel_name = rk.name;
+    req.source_ref = rk.source_ref;
+    req.global = rk.global;
+    req.local = rk.local;
+    req.arguments = t->job.kernel.arguments;
+    req.device_name = t->job.device.name;
+    req.repetitions = 1;
+    req.want_outputs = false;  // nothing to verify the reference against
+    EvaluationResult r = cb->evaluate(req);
+    if (!r.ok()) throw Error("reference kernel " + rk.name + " failed: " + r.message);
+    std::vector<Buffer> outs;
+    int k = 0;
+    for (const ArgumentSpec& a : t->job.kernel.arguments) {
+        if (a.role != ArgRole::output) continue;
+        int st;
+        if (a.type == ElementType::i32) {
+            std::vector<int32_t> h(a.length);
+            st = ktc_backend_read_output(cb->handle(), k, h.data(), h.size() * 4);
+            outs.emplace_back(std::move(h));
+        } else {
+            std::vector<float> h(a.length);
+            st = ktc_backend_read_output(cb->handle(), k, h.data(), h.size() * 4);
+            outs.emplace_back(std::move(h));
+        }
+        if (st != KTC_OK) throw Error("cannot read reference output " + std::to_string(k));
+        ++k;
+    }
+    t->ref_outputs = outs;
+    auto shared = std::make_shared<std::vector<Buffer>>(std::move(outs));
+    t->job.reference = [shared] { return *shared; };
+}
+
 void tune(ktc_tuner* t) {
     const auto tb = std::chrono::steady_clock::now();
     ensure_backends(t);
     ktc::trace_phase("tune: backends", tb);
+    if (t->ref_kernel && !t->ref_outputs) compute_reference_outputs(t);
     const SearchSpace& eff = effective(t);
     ktc::trace_phase("tune: + effective space", tb);
     std::vector<Backend*> bes;
@@ -684,6 +732,44 @@ int ktc_tuner_set_local_memory(ktc_tuner* t, const char* expr) {
 int ktc_tuner_add_argument(ktc_tuner* t, const ktc_arg* arg) {
     return guard([&] {
         t->job.kernel.arguments.push_back(arg_from_c(arg));
+        if (t->ref_kernel) t->ref_outputs.reset();  // recomputed for the new argument list
+        touched(t);
+    });
+}
+
+int ktc_tuner_set_reference_kernel(ktc_tuner* t, const char* source_ref, const char* name,
+                                   int ndim, const size_t* global, const size_t* local) {
+    return guard([&] {
+        if (ndim < 1 || ndim > 3) throw Error("reference kernel needs 1 to 3 dimensions");
+        ktc_tuner::RefKernel k;
+        k.source_ref = source_ref ? source_ref : "";
+        k.name = name ? name : "";
+        k.global.assign(global, global + ndim);
+        k.local.assign(local, local + ndim);
+        t->ref_kernel = k;
+        t->ref_outputs.reset();
+        t->job.reference = nullptr;
+        touched(t);
+    });
+}
+
+int ktc_tuner_set_reference_outputs(ktc_tuner* t, int n, const void* const* buffers,
+                                    const size_t* lengths, const int* types) {
+    return guard([&] {
+        std::vector<Buffer> refs;
+        for (int i = 0; i < n; ++i) {
+            if (types[i] == KTC_I32) {
+                const auto* p = static_cast<const int32_t*>(buffers[i]);
+                refs.emplace_back(std::vector<int32_t>(p, p + lengths[i]));
+            } else {
+                const auto* p = static_cast<const float*>(buffers[i]);
+                refs.emplace_back(std::vector<float>(p, p + lengths[i]));
+            }
+        }
+        t->ref_kernel.reset();
+        t->ref_outputs = std::move(refs);
+        auto shared = std::make_shared<std::vector<Buffer>>(*t->ref_outputs);
+        t->job.reference = [shared] { return *shared; };
         touched(t);
     });
 }

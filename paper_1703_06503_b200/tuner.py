@@ -156,6 +156,31 @@ class Tuner:
     def AddArgumentScalar(self, value, dtype: str = "i32"):
         self._argument(K.ARG_SCALAR, K.I32 if dtype == "i32" else K.F32, 0, value, "")
 
+    def SetReference(self, source_ref: str, name: str, global_size: Sequence[int],
+                     local_size: Sequence[int]) -> None:
+        """CLTune SetReference: a reference kernel (no tuning parameters), run
+        once on the device over the same arguments when Tune() starts; every
+        configuration is then verified on the device against its outputs."""
+        g, n = _arr(C.c_size_t, global_size)
+        l, _ = _arr(C.c_size_t, local_size)
+        K.check(self._lib.ktc_tuner_set_reference_kernel(self._h, source_ref.encode(),
+                                                         name.encode(), n, g, l))
+
+    def SetReferenceOutputs(self, outputs) -> None:
+        """Host reference outputs (numpy arrays, one per output argument)."""
+        import numpy as np
+
+        arrs = []
+        for o in outputs:
+            o = np.asarray(o)
+            arrs.append(np.ascontiguousarray(o, dtype=np.int32 if o.dtype == np.int32 else np.float32))
+        self._ref_keep = arrs
+        ptrs = (C.c_void_p * max(1, len(arrs)))(*[a.ctypes.data for a in arrs])
+        lens = (C.c_size_t * max(1, len(arrs)))(*[a.size for a in arrs])
+        types = (C.c_int * max(1, len(arrs)))(*[K.I32 if a.dtype == np.int32 else K.F32
+                                                 for a in arrs])
+        K.check(self._lib.ktc_tuner_set_reference_outputs(self._h, len(arrs), ptrs, lens, types))
+
     # ------------------------------------------------------------- strategy
     def UseFullSearch(self):
         K.check(self._lib.ktc_tuner_set_strategy(self._h, K.SEARCH_FULL, 1.0, 4.0, 0.4, 0.0, 0.4, 3))
