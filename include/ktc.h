@@ -116,6 +116,13 @@ int ktc_reset(ktc_ctx* ctx);
 int ktc_compile(const char* src, const char* const* opts, int nopts, void** cubin,
                 size_t* cubin_size, char* log, size_t log_cap);
 void ktc_free_host(void* p);
+/* The convolution family's direct code generator (the tuning-time default):
+ * emits the PTX of one configuration of kernels/conv.cu -- `defines` are its
+ * "NAME=VALUE" compile-time parameters plus "FS=<filter>" -- and compiles it
+ * with ptxas for sm_100a, entry "conv2d_k0".  No device needed.  `ptx`
+ * (optional) receives the PTX text (free with ktc_free_host). */
+int ktc_codegen_conv(const char* const* defines, int ndefines, void** cubin, size_t* cubin_size,
+                     char** ptx, char* log, size_t log_cap);
 
 int ktc_load(ktc_ctx* ctx, const void* cubin, size_t size, const char* kernel_name, ktc_fn** fn);
 void ktc_unload(ktc_fn* fn);

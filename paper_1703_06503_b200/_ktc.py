@@ -147,6 +147,8 @@ _SIGS = {
     "ktc_compile": (C.c_int, [C.c_char_p, C.POINTER(C.c_char_p), C.c_int, C.POINTER(_P),
                               C.POINTER(C.c_size_t), C.c_char_p, C.c_size_t]),
     "ktc_free_host": (None, [_P]),
+    "ktc_codegen_conv": (C.c_int, [C.POINTER(C.c_char_p), C.c_int, C.POINTER(_P),
+                                   C.POINTER(C.c_size_t), C.POINTER(_P), C.c_char_p, C.c_size_t]),
     "ktc_load": (C.c_int, [_P, _P, C.c_size_t, C.c_char_p, C.POINTER(_P)]),
     "ktc_unload": (None, [_P]),
     "ktc_set_symbol": (C.c_int, [_P, C.c_char_p, _P, C.c_size_t]),
@@ -269,6 +271,24 @@ def compile_source(src: str, options: list[str]) -> bytes:
     data = C.string_at(out, size.value)
     L.ktc_free_host(out)
     return data
+
+
+def codegen_conv(defines: list[str]) -> tuple[bytes, str]:
+    """The conv family's direct PTX generator + ptxas (no GPU): (cubin, ptx)."""
+    L = lib()
+    arr = (C.c_char_p * max(1, len(defines)))(*[d.encode() for d in defines])
+    out, ptx = C.c_void_p(), C.c_void_p()
+    size = C.c_size_t()
+    log = C.create_string_buffer(8192)
+    rc = L.ktc_codegen_conv(arr, len(defines), C.byref(out), C.byref(size), C.byref(ptx), log, 8192)
+    text = C.string_at(ptx).decode() if ptx.value else ""
+    if ptx.value:
+        L.ktc_free_host(ptx)
+    if rc != KTC_OK:
+        raise KtcError(rc, log.value.decode(errors="replace") + "\n" + text[-3000:])
+    data = C.string_at(out, size.value)
+    L.ktc_free_host(out)
+    return data, text
 
 
 def device_count() -> int:

@@ -92,8 +92,20 @@ std::string define(const char* name, long long v) {
     return std::string(name) + "=" + std::to_string(v);
 }
 
+// The conv family's code path: "ptx" (default) = the direct PTX generator
+// (ptxgen_conv.cpp, ptxas only), "nvrtc" = kernels/conv.cu through NVRTC.
+// KTC_CONV_CODEGEN overrides; both produce the same kernels.
 const KernelSource& conv_source() {
-    static const KernelSource s = split_source("conv.cu", kConvSource, "conv2d");
+    static const KernelSource s = [] {
+        const char* e = std::getenv("KTC_CONV_CODEGEN");
+        const std::string mode = e ? e : "ptx";
+        KernelSource k = split_source("conv.cu", kConvSource, "conv2d");
+        if (mode == "ptx") {
+            k.id = "ptxgen-conv#1|" + k.id;
+            k.ptx_generator = conv_ptx_module;
+        }
+        return k;
+    }();
     return s;
 }
 const KernelSource& gemm_source() {

@@ -1,6 +1,7 @@
 // nvrtc_pool.cpp -- see nvrtc_pool.hpp.
 #include "nvrtc_pool.hpp"
 
+#include <nvPTXCompiler.h>
 #include <nvrtc.h>
 #include <sys/stat.h>
 
@@ -129,6 +130,36 @@ CubinPtr nvrtc_compile(const std::string& src, const std::vector<std::string>& o
     return out;
 }
 
+CubinPtr ptx_compile(const std::string& ptx) {
+    auto out = std::make_shared<Cubin>();
+    auto t0 = std::chrono::steady_clock::now();
+    nvPTXCompilerHandle h = nullptr;
+    if (nvPTXCompilerCreate(&h, ptx.size(), ptx.c_str()) != NVPTXCOMPILE_SUCCESS) {
+        out->log = "nvPTXCompilerCreate failed";
+        return out;
+    }
+    std::vector<const char*> argv = {"--gpu-name=sm_100a", "-O3"};
+    const char* li = std::getenv("KTC_LINEINFO");
+    if (li && std::strcmp(li, "0") != 0) argv.push_back("--generate-line-info");
+    const nvPTXCompileResult rc = nvPTXCompilerCompile(h, int(argv.size()), argv.data());
+    size_t n = 0;
+    if (rc == NVPTXCOMPILE_SUCCESS) {
+        nvPTXCompilerGetCompiledProgramSize(h, &n);
+        out->image.resize(n);
+        nvPTXCompilerGetCompiledProgram(h, out->image.data());
+    } else {
+        nvPTXCompilerGetErrorLogSize(h, &n);
+        std::string log(n, '\0');
+        if (n) nvPTXCompilerGetErrorLog(h, log.data());
+        while (!log.empty() && (log.back() == '\0' || log.back() == '\n')) log.pop_back();
+        out->log = "ptxas: " + (log.empty() ? std::string("error ") + std::to_string(int(rc)) : log);
+    }
+    nvPTXCompilerDestroy(&h);
+    out->compile_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return out;
+}
+
 CompileService& CompileService::instance() {
     static CompileService* svc = new CompileService;  // intentionally leaked: workers outlive statics
     return *svc;
@@ -232,7 +263,20 @@ void CompileService::run_batch(Batch b) {
     auto compile_group = [&](const std::vector<Item*>& group) -> bool {
         std::vector<const Defines*> cfgs;
         for (Item* it : group) cfgs.push_back(&it->config);
-        CubinPtr c = nvrtc_compile(assemble(*b.src, cfgs), popts);
+        CubinPtr c;
+        if (b.src->ptx_generator) {
+            std::string ptx;
+            try {
+                ptx = b.src->ptx_generator(b.problem, cfgs, b.src->entry_base);
+            } catch (const std::exception& e) {
+                auto bad = std::make_shared<Cubin>();
+                bad->log = std::string("ptx generator: ") + e.what();
+                c = bad;
+            }
+            if (!c) c = ptx_compile(ptx);
+        } else {
+            c = nvrtc_compile(assemble(*b.src, cfgs), popts);
+        }
         {
             std::lock_guard<std::mutex> lk(mu_);
             compile_ms_ += c->compile_ms;
@@ -442,6 +486,40 @@ extern "C" int ktc_compile(const char* src, const char* const* opts, int nopts, 
     if (log && log_cap) std::snprintf(log, log_cap, "%s", c->log.c_str());
     if (!c->ok()) {
         set_error("NVRTC: " + c->log.substr(0, 2000));
+        *cubin = nullptr;
+        *cubin_size = 0;
+        return KTC_ERR_NVRTC;
+    }
+    *cubin = std::malloc(c->image.size());
+    std::memcpy(*cubin, c->image.data(), c->image.size());
+    *cubin_size = c->image.size();
+    return KTC_OK;
+}
+
+extern "C" int ktc_codegen_conv(const char* const* defines, int ndefines, void** cubin,
+                                size_t* cubin_size, char** ptx, char* log, size_t log_cap) {
+    Defines problem, config;
+    for (int i = 0; i < ndefines; ++i) {
+        std::string d = defines[i];
+        if (d.rfind("-D", 0) == 0) d = d.substr(2);
+        (d.rfind("FS=", 0) == 0 ? problem : config).push_back(d);
+    }
+    std::string text;
+    try {
+        text = conv_ptx_module(problem, {&config}, "conv2d");
+    } catch (const std::exception& e) {
+        if (log && log_cap) std::snprintf(log, log_cap, "%s", e.what());
+        set_error(e.what());
+        return KTC_ERR_INVALID;
+    }
+    if (ptx) {
+        *ptx = static_cast<char*>(std::malloc(text.size() + 1));
+        std::memcpy(*ptx, text.c_str(), text.size() + 1);
+    }
+    CubinPtr c = ptx_compile(text);
+    if (log && log_cap) std::snprintf(log, log_cap, "%s", c->log.c_str());
+    if (!c->ok()) {
+        set_error(c->log.substr(0, 2000));
         *cubin = nullptr;
         *cubin_size = 0;
         return KTC_ERR_NVRTC;

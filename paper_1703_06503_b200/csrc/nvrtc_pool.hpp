@@ -21,6 +21,7 @@
 #include <condition_variable>
 #include <cstdint>
 #include <deque>
+#include <functional>
 #include <future>
 #include <map>
 #include <memory>
@@ -41,6 +42,9 @@ struct Cubin {
 using CubinPtr = std::shared_ptr<const Cubin>;
 
 // A family's source split at the body marker.
+// Defines are "NAME=VALUE" strings.
+using Defines = std::vector<std::string>;
+
 struct KernelSource {
     std::string id;          // identity (name + content hash)
     std::string prelude;
@@ -50,6 +54,11 @@ struct KernelSource {
     // configuration passed as -D options.
     bool batchable = true;
     std::string fixed_entry;
+    // Direct code generation (no NVRTC): emits the PTX module of a batch
+    // (entries entry_base_k<i>), compiled by ptxas in process.
+    std::function<std::string(const Defines& problem, const std::vector<const Defines*>& configs,
+                              const std::string& entry_base)>
+        ptx_generator;
 };
 KernelSource split_source(const std::string& name, const std::string& text,
                           const std::string& entry_base);
@@ -64,11 +73,16 @@ struct CompiledKernel {
 };
 using KernelPtr = std::shared_ptr<const CompiledKernel>;
 
-// Defines are "NAME=VALUE" strings.
-using Defines = std::vector<std::string>;
 
 // Raw NVRTC compile of `src` with extra options (fixed arch/std options added).
 CubinPtr nvrtc_compile(const std::string& src, const std::vector<std::string>& opts);
+
+// ptxas (nvPTXCompiler, in process) of a PTX module for sm_100a.
+CubinPtr ptx_compile(const std::string& ptx);
+
+// PTX generator of the convolution family (ptxgen_conv.cpp).
+std::string conv_ptx_module(const Defines& problem, const std::vector<const Defines*>& configs,
+                            const std::string& entry_base);
 
 class CompileService {
   public:

@@ -138,3 +138,20 @@ def test_conv_unrolled_rows_issue_packed_ffma2(built, tmp_path):
     assert (n2, n1) == (880, 176)
     sass0 = _sass(K.compile_source((KERNELS / "conv.cu").read_text(), opts + ["-DCF2=0"]), tmp_path)
     assert len(re.findall(r"\bFFMA2\b", sass0)) == 0
+
+
+@pytest.mark.parametrize("cfg", [
+    (3, 32, 8, 1, 8, 0, 1, 0, 1), (7, 32, 16, 2, 4, 2, 2, 1, 1), (5, 64, 8, 4, 4, 1, 4, 1, 0),
+    (9, 8, 64, 8, 8, 2, 4, 0, 1), (3, 16, 16, 8, 2, 1, 8, 0, 1), (11, 16, 8, 4, 4, 2, 4, 0, 1),
+    (11, 8, 8, 2, 2, 2, 2, 1, 0), (3, 64, 8, 8, 8, 2, 8, 1, 1),
+])
+def test_conv_ptx_codegen_compiles_and_matches_fma_counts(built, tmp_path, cfg):
+    """The direct PTX generator (the conv family's tuning-time code path)
+    compiles every mode with ptxas and issues the same FFMA/FFMA2 as conv.cu."""
+    d = _conv_defines(*cfg)
+    gen, ptx = K.codegen_conv([x[2:] for x in d])
+    assert gen[:4] == b"\x7fELF" and ".entry conv2d_k0" in ptx
+    ref = K.compile_source((KERNELS / "conv.cu").read_text(), d)
+    count = lambda s, op: len(re.findall(rf"\b{op}\b", s))  # noqa: E731
+    sg, sr = _sass(gen, tmp_path), _sass(ref, tmp_path)
+    assert (count(sg, "FFMA2"), count(sg, "FFMA")) == (count(sr, "FFMA2"), count(sr, "FFMA"))
