@@ -196,12 +196,14 @@ void free_inputs(ktc_backend* be) {
     const Driver& d = driver();
     if (!be->ctx->sticky) {
         d.cuCtxSetCurrent(be->ctx->cu);
-        for (CUdeviceptr p : be->in->dev)
-            if (p) d.cuMemFree(p);
-        for (CUdeviceptr p : be->in->out)
-            if (p) d.cuMemFree(p);
-        for (CUdeviceptr p : be->in->ref)
-            if (p) d.cuMemFree(p);
+        d.cuStreamSynchronize(be->ctx->stream);  // blocks go back to the cache idle
+        const Inputs& I = *be->in;
+        for (size_t a = 0; a < I.dev.size(); ++a)
+            if (I.dev[a]) ctx_free(be->ctx, I.dev[a], a < I.bytes.size() ? I.bytes[a] : 0);
+        for (size_t k = 0; k < I.out.size(); ++k)
+            if (I.out[k]) ctx_free(be->ctx, I.out[k], I.out_count[k] * 4);
+        for (size_t k = 0; k < I.ref.size(); ++k)
+            if (I.ref[k]) ctx_free(be->ctx, I.ref[k], I.out_count[k] * 4);
     }
     be->in.reset();
 }
@@ -301,7 +303,7 @@ int build_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
     // error paths below release them via free_inputs.
     be->in = std::move(in);
     Inputs& I = *be->in;
-    auto alloc = [&](size_t bytes, CUdeviceptr* p) { return d.cuMemAlloc(p, bytes ? bytes : 4); };
+    auto alloc = [&](size_t bytes, CUdeviceptr* p) { return ctx_alloc(ctx, bytes ? bytes : 4, p); };
 
     if (fam == FAM_CONV) {
         I.X = int(I.args[0].value);
@@ -1147,7 +1149,7 @@ int ktc_backend_set_reference(ktc_backend* be, const ktc_request* req, int n_buf
             return KTC_ERR_INVALID;
         }
         if (!I.ref[k]) {
-            CUresult rc = d.cuMemAlloc(&I.ref[k], lengths[k] * 4);
+            CUresult rc = ctx_alloc(be->ctx, lengths[k] * 4, &I.ref[k]);
             if (rc != CUDA_SUCCESS) return fail_cu(be->ctx, rc, "cuMemAlloc(reference)");
         }
         CUresult rc = d.cuMemcpyHtoD(I.ref[k], buffers[k], lengths[k] * 4);

@@ -3,6 +3,7 @@
 
 #include <atomic>
 #include <chrono>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -288,6 +289,7 @@ static int setup_ctx(ktc_ctx* c) {
     rc = d.cuMemAlloc(&c->scratch, scratch);
     if (rc != CUDA_SUCCESS) return fail_cu(c, rc, "cuMemAlloc(scratch)");
     c->sticky = false;
+    c->epoch = ktc::primary_ctx_epoch();
     return KTC_OK;
 }
 
@@ -309,10 +311,48 @@ void ktc::trace_phase(const char* what, std::chrono::steady_clock::time_point si
 }
 extern "C" {
 
+}  // extern "C"
+CUresult ktc::ctx_alloc(ktc_ctx* ctx, size_t bytes, CUdeviceptr* p) {
+    if (!bytes) bytes = 4;
+    for (size_t i = 0; i < ctx->free_blocks.size(); ++i)
+        if (ctx->free_blocks[i].first == bytes) {
+            *p = ctx->free_blocks[i].second;
+            ctx->free_bytes -= bytes;
+            ctx->free_blocks.erase(ctx->free_blocks.begin() + long(i));
+            return CUDA_SUCCESS;
+        }
+    CUresult rc = driver().cuMemAlloc(p, bytes);
+    if (rc == CUDA_ERROR_OUT_OF_MEMORY && !ctx->free_blocks.empty()) {
+        for (auto& b : ctx->free_blocks) driver().cuMemFree(b.second);
+        ctx->free_blocks.clear();
+        ctx->free_bytes = 0;
+        rc = driver().cuMemAlloc(p, bytes);
+    }
+    return rc;
+}
+
+void ktc::ctx_free(ktc_ctx* ctx, CUdeviceptr p, size_t bytes) {
+    if (!p) return;
+    if (!bytes) bytes = 4;
+    constexpr size_t kCacheCap = size_t(2) << 30;
+    if (ctx->sticky) return;  // died with the context
+    if (ctx->free_bytes + bytes <= kCacheCap) {
+        ctx->free_blocks.emplace_back(bytes, p);
+        ctx->free_bytes += bytes;
+    } else {
+        driver().cuMemFree(p);
+    }
+}
+extern "C" {
+
 static void teardown_ctx(ktc_ctx* c, bool reset) {
     const Driver& d = driver();
     if (!c->cu) return;
     const auto t0 = std::chrono::steady_clock::now();
+    if (!reset)
+        for (auto& b : c->free_blocks) d.cuMemFree(b.second);
+    c->free_blocks.clear();
+    c->free_bytes = 0;
     d.cuCtxSetCurrent(c->cu);
     if (!reset) {
         for (CUevent e : c->events) d.cuEventDestroy(e);
@@ -338,6 +378,48 @@ static void teardown_ctx(ktc_ctx* c, bool reset) {
     c->cu = nullptr;
 }
 
+// Context pool: a closed context (stream, builtin module, verifier
+// scratch, L2-flush buffer, cached device blocks) is kept for the next
+// ktc_open of the same device, so a new tuning job pays none of that setup.
+// Contexts made before a primary-context reset are dropped (their resources
+// died with it).
+static std::mutex g_pool_mu;
+static std::vector<ktc_ctx*> g_pool;
+
+static ktc_ctx* take_pooled(int ordinal) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (size_t i = 0; i < g_pool.size(); ++i) {
+        ktc_ctx* c = g_pool[i];
+        if (c->ordinal != ordinal) continue;
+        g_pool.erase(g_pool.begin() + long(i));
+        if (c->epoch != ktc::primary_ctx_epoch()) {
+            driver().cuDevicePrimaryCtxRelease(c->dev);
+            delete c;
+            return nullptr;
+        }
+        driver().cuCtxSetCurrent(c->cu);
+        c->ref = 0;
+        c->ref_count = 0;
+        c->launches = 0;
+        return c;
+    }
+    return nullptr;
+}
+
+static bool pool_ctx(ktc_ctx* c) {
+    if (c->sticky || !c->cu || c->epoch != ktc::primary_ctx_epoch()) return false;
+    const char* e = std::getenv("KTC_CTX_POOL");
+    if (e && std::strcmp(e, "0") == 0) return false;
+    driver().cuCtxSetCurrent(c->cu);
+    if (driver().cuStreamSynchronize(c->stream) != CUDA_SUCCESS) return false;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    int same = 0;
+    for (ktc_ctx* p : g_pool) same += p->ordinal == c->ordinal;
+    if (same >= 2) return false;
+    g_pool.push_back(c);
+    return true;
+}
+
 int ktc_open(int ordinal, ktc_ctx** out) {
     *out = nullptr;
     const Driver& d = driver();
@@ -351,6 +433,10 @@ int ktc_open(int ordinal, ktc_ctx** out) {
         set_error("device ordinal " + std::to_string(ordinal) + " out of range (" +
                   std::to_string(count) + " devices)");
         return KTC_ERR_NO_DEVICE;
+    }
+    if (ktc_ctx* pooled = take_pooled(ordinal)) {
+        *out = pooled;
+        return KTC_OK;
     }
     auto* c = new ktc_ctx;
     c->ordinal = ordinal;
@@ -371,6 +457,7 @@ int ktc_open(int ordinal, ktc_ctx** out) {
 
 void ktc_close(ktc_ctx* ctx) {
     if (!ctx) return;
+    if (pool_ctx(ctx)) return;
     teardown_ctx(ctx, false);
     delete ctx;
 }

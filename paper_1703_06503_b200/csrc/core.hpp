@@ -44,6 +44,12 @@ struct ktc_ctx {
     ktc_limits limits{};
     bool sticky = false;   // a sticky CUDA error poisoned the context
     long long launches = 0;  // kernels launched through this context
+    // Device blocks kept for reuse (exact size match): a new job over the
+    // same problem on a pooled context gets its buffers back without
+    // cuMemAlloc/cuMemFree (ktc::ctx_alloc / ctx_free).
+    std::vector<std::pair<size_t, CUdeviceptr>> free_blocks;
+    size_t free_bytes = 0;
+    unsigned epoch = 0;  // primary_ctx_epoch() when the resources were made
 };
 
 struct ktc_fn {
@@ -57,6 +63,10 @@ namespace ktc {
 // Thread-local last-error plumbing shared by every layer.
 void set_error(const std::string& msg);
 const std::string& last_error();
+
+// Device allocation through the context's block cache.
+CUresult ctx_alloc(ktc_ctx* ctx, size_t bytes, CUdeviceptr* p);
+void ctx_free(ktc_ctx* ctx, CUdeviceptr p, size_t bytes);
 
 // KTC_TRACE=1: phase timings of job setup / teardown on stderr (diagnostics).
 bool trace_on();
