@@ -123,6 +123,10 @@ void ktc_free_host(void* p);
  * (optional) receives the PTX text (free with ktc_free_host). */
 int ktc_codegen_conv(const char* const* defines, int ndefines, void** cubin, size_t* cubin_size,
                      char** ptx, char* log, size_t log_cap);
+/* The same for the SGEMM family (kernels/gemm.cu semantics, entry "gemm_k0";
+ * defines: the 14 parameters plus DBUF / OCC / F2). */
+int ktc_codegen_gemm(const char* const* defines, int ndefines, void** cubin, size_t* cubin_size,
+                     char** ptx, char* log, size_t log_cap);
 
 int ktc_load(ktc_ctx* ctx, const void* cubin, size_t size, const char* kernel_name, ktc_fn** fn);
 void ktc_unload(ktc_fn* fn);

@@ -149,6 +149,8 @@ _SIGS = {
     "ktc_free_host": (None, [_P]),
     "ktc_codegen_conv": (C.c_int, [C.POINTER(C.c_char_p), C.c_int, C.POINTER(_P),
                                    C.POINTER(C.c_size_t), C.POINTER(_P), C.c_char_p, C.c_size_t]),
+    "ktc_codegen_gemm": (C.c_int, [C.POINTER(C.c_char_p), C.c_int, C.POINTER(_P),
+                                   C.POINTER(C.c_size_t), C.POINTER(_P), C.c_char_p, C.c_size_t]),
     "ktc_load": (C.c_int, [_P, _P, C.c_size_t, C.c_char_p, C.POINTER(_P)]),
     "ktc_unload": (None, [_P]),
     "ktc_set_symbol": (C.c_int, [_P, C.c_char_p, _P, C.c_size_t]),
@@ -275,12 +277,21 @@ def compile_source(src: str, options: list[str]) -> bytes:
 
 def codegen_conv(defines: list[str]) -> tuple[bytes, str]:
     """The conv family's direct PTX generator + ptxas (no GPU): (cubin, ptx)."""
+    return _codegen("ktc_codegen_conv", defines)
+
+
+def codegen_gemm(defines: list[str]) -> tuple[bytes, str]:
+    """The SGEMM family's direct PTX generator + ptxas (no GPU): (cubin, ptx)."""
+    return _codegen("ktc_codegen_gemm", defines)
+
+
+def _codegen(fn: str, defines: list[str]) -> tuple[bytes, str]:
     L = lib()
     arr = (C.c_char_p * max(1, len(defines)))(*[d.encode() for d in defines])
     out, ptx = C.c_void_p(), C.c_void_p()
     size = C.c_size_t()
     log = C.create_string_buffer(8192)
-    rc = L.ktc_codegen_conv(arr, len(defines), C.byref(out), C.byref(size), C.byref(ptx), log, 8192)
+    rc = getattr(L, fn)(arr, len(defines), C.byref(out), C.byref(size), C.byref(ptx), log, 8192)
     text = C.string_at(ptx).decode() if ptx.value else ""
     if ptx.value:
         L.ktc_free_host(ptx)

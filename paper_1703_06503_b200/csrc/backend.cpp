@@ -108,8 +108,19 @@ const KernelSource& conv_source() {
     }();
     return s;
 }
+// The SGEMM family's code path: "ptx" (default) = ptxgen_gemm.cpp, "nvrtc"
+// = kernels/gemm.cu through NVRTC.  KTC_GEMM_CODEGEN overrides.
 const KernelSource& gemm_source() {
-    static const KernelSource s = split_source("gemm.cu", kGemmSource, "gemm");
+    static const KernelSource s = [] {
+        const char* e = std::getenv("KTC_GEMM_CODEGEN");
+        const std::string mode = e ? e : "ptx";
+        KernelSource k = split_source("gemm.cu", kGemmSource, "gemm");
+        if (mode == "ptx") {
+            k.id = "ptxgen-gemm#1|" + k.id;
+            k.ptx_generator = gemm_ptx_module;
+        }
+        return k;
+    }();
     return s;
 }
 const KernelSource& tf32_source() {

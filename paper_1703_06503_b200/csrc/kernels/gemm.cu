@@ -397,7 +397,9 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
                     float c[VWN];
                     vload_g<VWN>(c, Cin + idx);
 #pragma unroll
-                    for (int q = 0; q < VWN; ++q) s[q] = alpha * acc[mi * VWM + e][ni * VWN + q] + beta * c[q];
+                    // Explicit fmaf: the contraction is fixed (NVVM would
+                    // otherwise pick either product per configuration).
+                    for (int q = 0; q < VWN; ++q) s[q] = fmaf(alpha, acc[mi * VWM + e][ni * VWN + q], beta * c[q]);
                 } else {
 #pragma unroll
                     for (int q = 0; q < VWN; ++q) s[q] = alpha * acc[mi * VWM + e][ni * VWN + q];

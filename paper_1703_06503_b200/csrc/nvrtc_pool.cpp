@@ -496,8 +496,8 @@ extern "C" int ktc_compile(const char* src, const char* const* opts, int nopts, 
     return KTC_OK;
 }
 
-extern "C" int ktc_codegen_conv(const char* const* defines, int ndefines, void** cubin,
-                                size_t* cubin_size, char** ptx, char* log, size_t log_cap) {
+static int codegen(bool gemm, const char* const* defines, int ndefines, void** cubin,
+                   size_t* cubin_size, char** ptx, char* log, size_t log_cap) {
     Defines problem, config;
     for (int i = 0; i < ndefines; ++i) {
         std::string d = defines[i];
@@ -506,7 +506,8 @@ extern "C" int ktc_codegen_conv(const char* const* defines, int ndefines, void**
     }
     std::string text;
     try {
-        text = conv_ptx_module(problem, {&config}, "conv2d");
+        text = gemm ? gemm_ptx_module(problem, {&config}, "gemm")
+                    : conv_ptx_module(problem, {&config}, "conv2d");
     } catch (const std::exception& e) {
         if (log && log_cap) std::snprintf(log, log_cap, "%s", e.what());
         set_error(e.what());
@@ -528,4 +529,14 @@ extern "C" int ktc_codegen_conv(const char* const* defines, int ndefines, void**
     std::memcpy(*cubin, c->image.data(), c->image.size());
     *cubin_size = c->image.size();
     return KTC_OK;
+}
+
+extern "C" int ktc_codegen_conv(const char* const* defines, int ndefines, void** cubin,
+                                size_t* cubin_size, char** ptx, char* log, size_t log_cap) {
+    return codegen(false, defines, ndefines, cubin, cubin_size, ptx, log, log_cap);
+}
+
+extern "C" int ktc_codegen_gemm(const char* const* defines, int ndefines, void** cubin,
+                                size_t* cubin_size, char** ptx, char* log, size_t log_cap) {
+    return codegen(true, defines, ndefines, cubin, cubin_size, ptx, log, log_cap);
 }

@@ -80,8 +80,10 @@ CubinPtr nvrtc_compile(const std::string& src, const std::vector<std::string>& o
 // ptxas (nvPTXCompiler, in process) of a PTX module for sm_100a.
 CubinPtr ptx_compile(const std::string& ptx);
 
-// PTX generator of the convolution family (ptxgen_conv.cpp).
+// PTX generators of the convolution and SGEMM families (ptxgen_*.cpp).
 std::string conv_ptx_module(const Defines& problem, const std::vector<const Defines*>& configs,
+                            const std::string& entry_base);
+std::string gemm_ptx_module(const Defines& problem, const std::vector<const Defines*>& configs,
                             const std::string& entry_base);
 
 class CompileService {

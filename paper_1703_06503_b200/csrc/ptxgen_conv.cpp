@@ -12,7 +12,7 @@
 // Structure of the emitted entry (see conv.cu for the semantics):
 //   prologue   tile origin, thread offsets
 //   LOCAL = 0  sliding windows read with ld.global.nc (vector width VW)
-//   LOCAL = 1  cooperative halo copy into shared memory (fully unrolled),
+//   LOCAL = 1  cooperative halo copy into shared memory (4 copies per trip),
 //              bar.sync, windows from shared memory
 //   LOCAL = 2  one thread: mbarrier init + expect_tx + TMA 2D boxes per panel;
 //              bounded try_wait (trap on timeout); windows from the panels
@@ -202,12 +202,20 @@ std::string emit_entry(const ConvGen& g, const std::string& name) {
             x.op("shl.b64 " + d1 + ", " + d1 + ", 2");
             x.op("add.u64 " + gb + ", " + dImg + ", " + d1);
         }
+        // conv.cu's `#pragma unroll 4` loop: up to four guarded copies per
+        // trip of a rolled loop (four loads in flight, bounded code size).
         const int iters = (TOT + NT - 1) / NT;
-        for (int it = 0; it < iters; ++it) {
+        const int U = std::min(iters, 4);
+        const std::string base_e = x.r();
+        x.op("mov.u32 " + base_e + ", " + tid);
+        const std::string top = x.label(), out = x.label();
+        const bool looped = iters > U;
+        if (looped) x.lab(top);
+        for (int u = 0; u < U; ++u) {
             const std::string skip = x.label();
             const std::string e = x.r();
-            x.op("add.u32 " + e + ", " + tid + ", " + imm((long long)it * NT));
-            if ((long long)(it + 1) * NT > TOT) {
+            x.op("add.u32 " + e + ", " + base_e + ", " + imm((long long)u * NT));
+            if (looped || (long long)(u + 1) * NT > TOT) {
                 const std::string pe = x.p();
                 x.op("setp.ge.u32 " + pe + ", " + e + ", " + imm(TOT));
                 x.op("@" + pe + " bra " + skip);
@@ -252,6 +260,13 @@ std::string emit_entry(const ConvGen& g, const std::string& name) {
             x.lab(done);
             x.lab(skip);
         }
+        if (looped) {
+            const std::string pl = x.p();
+            x.op("add.u32 " + base_e + ", " + base_e + ", " + imm((long long)U * NT));
+            x.op("setp.lt.u32 " + pl + ", " + base_e + ", " + imm(TOT));
+            x.op("@" + pl + " bra " + top);
+        }
+        x.lab(out);
         x.op("bar.sync 0");
         rowbase = x.r();
         x.op("mad.lo.u32 " + rowbase + ", " + ty + ", " + imm((long long)g.YWPT * g.SP * 4) + ", " +

@@ -155,3 +155,21 @@ def test_conv_ptx_codegen_compiles_and_matches_fma_counts(built, tmp_path, cfg):
     count = lambda s, op: len(re.findall(rf"\b{op}\b", s))  # noqa: E731
     sg, sr = _sass(gen, tmp_path), _sass(ref, tmp_path)
     assert (count(sg, "FFMA2"), count(sg, "FFMA")) == (count(sr, "FFMA2"), count(sr, "FFMA"))
+
+
+@pytest.mark.parametrize("row", [(128, 128, 16, 16, 16, 1, 1, 32, 16, 1, 0, 2, 1, 8),
+                                 (16, 16, 16, 8, 8, 0, 0, 8, 8, 0, 0, 1, 1, 2),
+                                 (64, 32, 64, 8, 32, 1, 0, 16, 8, 0, 1, 8, 1, 2),
+                                 (64, 64, 32, 16, 8, 1, 1, 32, 8, 0, 1, 4, 4, 8)])
+@pytest.mark.parametrize("dbuf", [0, 1])
+def test_gemm_ptx_codegen_matches_instruction_mix(built, tmp_path, row, dbuf):
+    """ptxgen_gemm emits the gemm.cu kernel: same FFMA2 / FFMA / cp.async counts."""
+    names = "MWG NWG KWG MDIMC NDIMC SA SB MDIMA NDIMB STRM STRN VWM VWN KWI".split()
+    d = [f"{k}={v}" for k, v in zip(names, row)] + [f"DBUF={dbuf}", "OCC=1", "F2=1"]
+    gen, ptx = K.codegen_gemm(d)
+    assert gen[:4] == b"\x7fELF" and ".entry gemm_k0" in ptx
+    ref = K.compile_source((KERNELS / "gemm.cu").read_text(), ["-D" + x for x in d])
+    count = lambda s, op: len(re.findall(rf"\b{op}\b", s))  # noqa: E731
+    sg, sr = _sass(gen, tmp_path), _sass(ref, tmp_path)
+    for op in ("FFMA2", "FFMA", "LDGSTS"):
+        assert count(sg, op) == count(sr, op), op
