@@ -303,3 +303,28 @@ def test_prune_factor_early_out_keeps_winner_and_verification(built):
     _, best_f = full.GetBestResult()
     _, best_p = pruned.GetBestResult()
     assert abs(best_p - best_f) / best_f < 0.05, (best_f, best_p)
+
+
+def test_sharded_executor_two_workers_on_one_device(built):
+    """run_tuning_sharded with two device workers (both on cuda:0 here; one per
+    GPU on a multi-GPU box): every unit evaluated once and verified, rows in
+    unit order with running bests, best = first minimum (CachedEvaluator's
+    strict <, search.hpp:203-208)."""
+    t = pkg.Tuner.conv(1024, 512, 5, devices=[0, 0])
+    _, _, n = t.space_counts()
+    units = list(range(0, n, 41))
+    t.SetSubset(units)
+    t.SetVerification(True)
+    t.Tune()
+    rows = t.rows()
+    assert [r.space_index for r in rows] == units
+    assert [r.step for r in rows] == list(range(1, len(units) + 1))
+    assert all(r.status == "ok" and r.verified == "pass" for r in rows)
+    times = [r.time_ms for r in rows]
+    best_i = min(range(len(times)), key=lambda i: (times[i], i))
+    cfg, ms = t.GetBestResult()
+    assert cfg == rows[best_i].config and ms == times[best_i]
+    run_best = None
+    for r in rows:
+        run_best = r.time_ms if run_best is None else min(run_best, r.time_ms)
+        assert r.best_so_far == run_best
