@@ -587,16 +587,6 @@ int gemm_occ_policy() {
     return v;
 }
 
-// Register fragment double buffering in the K loop (gemm.cu FRAG).
-// KTC_GEMM_FRAG overrides.
-int gemm_frag_policy() {
-    static const int v = [] {
-        const char* e = std::getenv("KTC_GEMM_FRAG");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-
 // Packed FFMA2 outer products (gemm.cu F2); KTC_GEMM_F2 overrides.
 int gemm_f2_policy() {
     static const int v = [] {
@@ -656,7 +646,6 @@ bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
                       2 * size_t(tile_bytes) <= be->ctx->limits.smem_per_block_optin;
     p->config.push_back(define("DBUF", dbuf ? 1 : 0));
     p->config.push_back(define("OCC", gemm_occ_policy()));
-    p->config.push_back(define("FRAG", gemm_frag_policy()));
     p->config.push_back(define("F2", gemm_f2_policy()));
     p->smem = dbuf ? 2 * tile_bytes : tile_bytes;
     p->compile_cost = unrolled_cost(double((MWG / MDIMC) * (NWG / NDIMC) * KWI) + 64.0);
@@ -742,8 +731,6 @@ bool plan_gemm_tf32(ktc_backend* be, const ktc_request* r, Plan* p, std::string*
     }
     p->ksrc = &tf32_source();
     p->config = {define("BN", BN), define("BK", BK), define("STAGES", STAGES)};
-    if (const char* v = std::getenv("KTC_TF32_DESC_VARIANT"))  // layout experiments
-        p->config.push_back(define("DESC_VARIANT", std::atoi(v)));
     p->smem = unsigned(STAGES * 4 * BK * (128 + BN) + 2048);
     if (p->smem > be->ctx->limits.smem_per_block_optin) {
         *why = "needs " + std::to_string(p->smem) + " bytes of shared memory";

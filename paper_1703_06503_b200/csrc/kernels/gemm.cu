@@ -159,10 +159,6 @@ __device__ __forceinline__ void outer_product_t(float (&acc)[MI][NJ], const floa
 // as an estimate of the live registers (accumulators + one A/B fragment +
 // addressing, + staging registers without DBUF) allows; OCC=0 leaves ptxas
 // the whole 255-register budget.
-#ifndef FRAG  // host-chosen (backend.cpp plan_gemm): register fragment double buffering
-#define FRAG 0
-#define KTC_FRAG_DEFAULT
-#endif
 #ifndef F2  // host-chosen: packed FFMA2 outer products
 #define F2 1
 #define KTC_F2_DEFAULT
@@ -172,7 +168,7 @@ __device__ __forceinline__ void outer_product_t(float (&acc)[MI][NJ], const floa
 #define OCC 0
 #define KTC_OCC_DEFAULT
 #endif
-#define EST_REGS (MWI * NWI + (1 + FRAG) * (MWI + NWI) + 40 + (DBUF ? 0 : STAGE_REGS * STAGE_AHEAD))
+#define EST_REGS (MWI * NWI + (MWI + NWI) + 40 + (DBUF ? 0 : STAGE_REGS * STAGE_AHEAD))
 #define MINB_RAW (65536 / (NT * EST_REGS))
 #define MINB (OCC == 0 || MINB_RAW < 1 ? 1 : (MINB_RAW > 16 ? 16 : MINB_RAW))
 
@@ -346,22 +342,6 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
         bt = blm + DBUF * buf * KWG * NWG;
 #endif
 
-#if FRAG
-        // Register fragments double-buffered across k: the A/B vectors of
-        // step k+1 are loaded while the outer product of step k runs (the
-        // next tile's first fragment is loaded after its barrier, above).
-        float fa[2][MWI], fb[2][NWI];
-        load_frag(fa[0], fb[0], 0);
-#pragma unroll 1
-        for (int kw = 0; kw < KWG; kw += KWI) {
-#pragma unroll
-            for (int ki = 0; ki < KWI; ++ki) {
-                const int k = kw + ki;
-                if (ki + 1 < KWI || kw + KWI < KWG) load_frag(fa[(ki + 1) & 1], fb[(ki + 1) & 1], k + 1);
-                outer_product(acc, fa[ki & 1], fb[ki & 1]);
-            }
-        }
-#else
 #pragma unroll 1
         for (int kw = 0; kw < KWG; kw += KWI) {
 #pragma unroll
@@ -371,7 +351,6 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
                 outer_product(acc, a, b);
             }
         }
-#endif
 #if !DBUF && (SA || SB)
         __syncthreads();
 #if !STAGE_AHEAD
@@ -443,10 +422,6 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
 #ifdef KTC_F2_DEFAULT
 #undef F2
 #undef KTC_F2_DEFAULT
-#endif
-#ifdef KTC_FRAG_DEFAULT
-#undef FRAG
-#undef KTC_FRAG_DEFAULT
 #endif
 #ifdef KTC_DBUF_DEFAULT
 #undef DBUF

@@ -2,7 +2,7 @@
 //
 // Emits, for one configuration, the kernel kernels/gemm.cu describes (CLTune
 // semantics of MWG/NWG/KWG, MDIMC/NDIMC, MDIMA/NDIMB, KWI, VWM/VWN, STRM/STRN,
-// SA/SB, plus the host switches DBUF / OCC / F2; FRAG must be 0) as PTX, so
+// SA/SB, plus the host switches DBUF / OCC / F2) as PTX, so
 // the tuning-time compile is ptxas only.  Same memory traffic, same
 // per-output FMA order (k ascending; alpha*acc, or gemm.cu's explicit
 // fmaf(alpha, acc, beta*c)) -> outputs bit-identical to the NVRTC build
@@ -62,7 +62,6 @@ GemmGen parse(const Defines& c) {
     g.DBUF = int(dv(c, "DBUF", false, 0));
     g.OCC = int(dv(c, "OCC", false, 0));
     g.F2 = int(dv(c, "F2", false, 1));
-    if (dv(c, "FRAG", false, 0) != 0) throw std::runtime_error("ptxgen: FRAG=1 is not generated");
     return g;
 }
 
