@@ -12,7 +12,7 @@
 //         BN/32 boxes, SWIZZLE_128B: each box is BK rows of 128 B, i.e. the
 //         canonical MN-major SW128 atom (8 K-rows x 128 B) stacked along K;
 //   ring  STAGES stages of A+B, full/empty mbarriers per stage;
-//   MMA   one elected thread issues tcgen05.mma.cta_group::1.kind::tf32
+//   MMA   one elected lane of warp 1 issues tcgen05.mma.cta_group::1.kind::tf32
 //         (M=128, N=BN, K=8) for each 8-row K group, accumulating into a
 //         128-lane x BN-column fp32 TMEM tile; tcgen05.commit releases the
 //         stage and finally signals the epilogue;
@@ -156,40 +156,52 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const u32 tmem = *tmem_slot;
 
-    if (warp == 0 && lane == 0) {
+    // Warp 0 produces, warp 1 issues the MMAs: one elected lane does the
+    // work, the rest of the warp stays converged with it (__syncwarp per
+    // K-block) instead of spinning on the accumulator barrier, which would
+    // split the warp and steal issue slots from the elected lane.
+    if (warp == 0) {
         // ---- TMA producer ----
         for (int kb = 0; kb < kblocks; ++kb) {
-            const int s = kb % STAGES;
-            const u32 phase = (u32)((kb / STAGES) & 1);
-            mbar_wait(empty0 + 8 * s, phase ^ 1u);
-            const u32 full = full0 + 8 * s;
-            mbar_expect_tx(full, STAGE_BYTES);
-            const u32 sa = smem_u32(smem + s * STAGE_BYTES);
-            const u32 sb = sa + A_STAGE_BYTES;
+            if (lane == 0) {
+                const int s = kb % STAGES;
+                const u32 phase = (u32)((kb / STAGES) & 1);
+                mbar_wait(empty0 + 8 * s, phase ^ 1u);
+                const u32 full = full0 + 8 * s;
+                mbar_expect_tx(full, STAGE_BYTES);
+                const u32 sa = smem_u32(smem + s * STAGE_BYTES);
+                const u32 sb = sa + A_STAGE_BYTES;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) tma_load_2d(sa + j * A_BOX_BYTES, &tmap_a, full, m0 + 32 * j, kb * BK);
+                for (int j = 0; j < 4; ++j)
+                    tma_load_2d(sa + j * A_BOX_BYTES, &tmap_a, full, m0 + 32 * j, kb * BK);
 #pragma unroll
-            for (int j = 0; j < BN / 32; ++j)
-                tma_load_2d(sb + j * A_BOX_BYTES, &tmap_b, full, n0 + 32 * j, kb * BK);
-        }
-    } else if (warp == 1 && lane == 0) {
-        // ---- MMA issuer (single thread) ----
-        for (int kb = 0; kb < kblocks; ++kb) {
-            const int s = kb % STAGES;
-            mbar_wait(full0 + 8 * s, (u32)((kb / STAGES) & 1));
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const u32 sa = smem_u32(smem + s * STAGE_BYTES);
-            const u32 sb = sa + A_STAGE_BYTES;
-#pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
-                // K = 8 per MMA = two 4-row groups of 512 B.
-                const u64 ad = umma_desc(sa + kk * 1024, A_BOX_BYTES, 512);
-                const u64 bd = umma_desc(sb + kk * 1024, A_BOX_BYTES, 512);
-                umma_tf32(tmem, ad, bd, make_idesc(BN), (kb | kk) != 0 ? 1u : 0u);
+                for (int j = 0; j < BN / 32; ++j)
+                    tma_load_2d(sb + j * A_BOX_BYTES, &tmap_b, full, n0 + 32 * j, kb * BK);
             }
-            umma_commit(empty0 + 8 * s);  // stage reusable once these MMAs retire
+            __syncwarp();
         }
-        umma_commit(accb);  // accumulator complete
+    } else if (warp == 1) {
+        // ---- MMA issuer (one elected thread) ----
+        for (int kb = 0; kb < kblocks; ++kb) {
+            if (lane == 0) {
+                const int s = kb % STAGES;
+                mbar_wait(full0 + 8 * s, (u32)((kb / STAGES) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const u32 sa = smem_u32(smem + s * STAGE_BYTES);
+                const u32 sb = sa + A_STAGE_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < BK / 8; ++kk) {
+                    // K = 8 per MMA = two 4-row groups of 512 B.
+                    const u64 ad = umma_desc(sa + kk * 1024, A_BOX_BYTES, 512);
+                    const u64 bd = umma_desc(sb + kk * 1024, A_BOX_BYTES, 512);
+                    umma_tf32(tmem, ad, bd, make_idesc(BN), (kb | kk) != 0 ? 1u : 0u);
+                }
+                umma_commit(empty0 + 8 * s);  // stage reusable once these MMAs retire
+            }
+            __syncwarp();
+        }
+        if (lane == 0) umma_commit(accb);  // accumulator complete
+        __syncwarp();
     }
 
     // ---- epilogue: all warps ----
