@@ -214,16 +214,17 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
     x.op("mul.wide.u32 " + rMb + ", " + rM + ", 4");
     x.op("mul.wide.u32 " + rNb + ", " + rN + ", 4");
 
-    // Global address of copy element (kk0 + l1*KW + ki, vector mvv) of
-    // operand c: base + (kk0 + l1*KW + ki) * ld + (o0 + mvv*VW) * 4.
-    auto copy_vec = [&](Copy& c, int i) -> std::pair<std::string, long long> {
-        // (mv register, constant part): STR ? l0 + i*DIM : i + l0*MV
+    // Copy element (row kk0 + l1*KW + ki, vector mv) of operand c lives at
+    // base + (kk0 + l1*KW + ki) * ld * 4 + (o0 + mv*VW) * 4 in global memory
+    // and at buf + ((l1*KW + ki) * WG + mv*VW) * 4 in the staged tile.
+    // Vector index copied by this thread's i-th copy: STR ? l0 + i*DIM : i + l0*MV.
+    auto copy_vec = [&](Copy& c, int i) -> std::string {
         const std::string mv = x.r();
         if (c.STR) x.op("add.u32 " + mv + ", " + c.l0 + ", " + imm((long long)i * c.DIM));
         else x.op("mad.lo.u32 " + mv + ", " + c.l0 + ", " + imm(c.MV) + ", " + imm(i));
-        return {mv, 0};
+        return mv;
     };
-    // Row (in K) base pointer of operand c's copy for K-tile kk0 (u32 reg).
+    // Global address of copy (ki, mv) of operand c for K-tile kk0.
     auto copy_gaddr = [&](Copy& c, bool isA, const std::string& kk0, int ki,
                           const std::string& mv) -> std::string {
         const std::string row = x.r(), d1 = x.d(), col = x.r(), d2 = x.d(), a = x.d();
@@ -248,7 +249,7 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
         return t;
     };
 
-    // cp.async issue of K-tile kk0 into buffer `bufoff` (byte offset reg incl. sbase+sm_off).
+    // cp.async of K-tile kk0 into the tiles at shared addresses buf_a / buf_b.
     auto issue = [&](const std::string& kk0, const std::string& buf_a, const std::string& buf_b) {
         for (Copy* c : {&ca, &cb}) {
             if (!c->on) continue;
@@ -257,7 +258,7 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
             if (!c->copies.empty()) x.op("@!" + c->copies + " bra " + skip);
             for (int ki = 0; ki < c->KW; ++ki)
                 for (int i = 0; i < c->MV; ++i) {
-                    const std::string mv = copy_vec(*c, i).first;
+                    const std::string mv = copy_vec(*c, i);
                     const std::string ga = copy_gaddr(*c, isA, kk0, ki, mv);
                     const std::string sa = copy_saddr(*c, isA ? buf_a : buf_b, ki, mv);
                     if (c->VW == 1) {
@@ -288,7 +289,7 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
             if (!c->copies.empty()) x.op("@!" + c->copies + " bra " + skip);
             for (int ki = 0; ki < c->KW; ++ki)
                 for (int i = 0; i < c->MV; ++i) {
-                    const std::string mv = copy_vec(*c, i).first;
+                    const std::string mv = copy_vec(*c, i);
                     const std::string ga = copy_gaddr(*c, isA, kk0, ki, mv);
                     std::vector<std::string> dst(regs.begin() + (ki * c->MV + i) * c->VW,
                                                  regs.begin() + (ki * c->MV + i + 1) * c->VW);
@@ -306,7 +307,7 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
             if (!c->copies.empty()) x.op("@!" + c->copies + " bra " + skip);
             for (int ki = 0; ki < c->KW; ++ki)
                 for (int i = 0; i < c->MV; ++i) {
-                    const std::string mv = copy_vec(*c, i).first;
+                    const std::string mv = copy_vec(*c, i);
                     const std::string sa = copy_saddr(*c, isA ? buf_a : buf_b, ki, mv);
                     std::vector<std::string> src(regs.begin() + (ki * c->MV + i) * c->VW,
                                                  regs.begin() + (ki * c->MV + i + 1) * c->VW);
