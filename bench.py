@@ -6,12 +6,13 @@ Workload (BASELINE.json configs[0], the reference's own CPU-runnable case):
 tuning the paper's 2D-convolution space for a 3x3 filter on an 8192x4096
 fp32 image, every configuration verified against the reference output.
 A *step* is one chunk of CHUNK configurations per GPU (weak scaling): each
-configuration is NVRTC-compiled for sm_100a, loaded, launched once to warm
+configuration is compiled for sm_100a (direct PTX generation + in-process
+ptxas), loaded, launched once to warm
 up and 3 timed times (CUDA events, L2 flushed before each, best of 3) and
 its output verified on the device against the bit-exact device reference.
 
   value  configurations evaluated per second, all GPUs (inputs resident in
-         HBM; cold NVRTC cache: every configuration compiled for the first
+         HBM; cold compile cache: every configuration compiled for the first
          time inside the timed region); max over ranks of the step time
   e2e    the same through the public API (Tuner, a fresh job per step):
          host materializes the inputs, H2D copy of the image and taps, D2H
@@ -328,8 +329,8 @@ def main():
     peaks = load_peaks()
 
     line = {
-        "metric": "conv2d 3x3 8192x4096 fp32 tuning throughput (configs evaluated/s, NVRTC "
-                  "compile + launch + time + device verify)",
+        "metric": "conv2d 3x3 8192x4096 fp32 tuning throughput (configs evaluated/s: "
+                  "sm_100a compile + launch + time + device verify)",
         "value": value, "unit": "configs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
