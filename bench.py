@@ -300,7 +300,7 @@ def main():
     ok = sum(1 for r in all_rows if r.status == "ok" and r.verified == "pass")
     failed_verify = sum(1 for r in all_rows if r.verified == "fail")
 
-    # warm NVRTC cache: the same units again (every cubin cached)
+    # warm compile cache: the same units again (every cubin cached)
     t0 = time.perf_counter()
     tuner.Tune()
     warm = max_over_ranks(world, time.perf_counter() - t0)
