@@ -1,7 +1,7 @@
 """Sustained-time A/B of conv kernel variants (run under gpurun; env knobs select the variant).
 
 For each filter: the 12 fastest configurations of the round-1b full search
-(profiles/sweep_r01b), timed two ways as bench.py does: best of 10 flushed
+(profiles/sweep_r01c), timed two ways as bench.py does: best of 10 flushed
 launches, and the mean of 30 back-to-back launches (the roofline figure).
 
   KTC_CONV_OSTREAM=0 python tools/conv_sustained_ab.py --out gpurun_out/os0.json
@@ -20,7 +20,7 @@ sys.path.insert(0, str(ROOT))
 
 def top(f, n):
     rows = [(r["config"], float(r["time_ms"])) for r in
-            csv.DictReader(open(ROOT / "profiles" / "sweep_r01b" / f"conv_f{f}_replay.csv"))]
+            csv.DictReader(open(ROOT / "profiles" / "sweep_r01c" / f"conv_f{f}_replay.csv"))]
     return [c for c, _ in sorted(rows, key=lambda r: r[1])[:n]]
 
 
