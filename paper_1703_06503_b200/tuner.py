@@ -265,6 +265,26 @@ class Tuner:
                 message=msg.value.decode()))
         return out
 
+    # CLTune reporting names
+    def SetNumRuns(self, n: int):
+        """CLTune's name for the timed repetitions per configuration (best of n)."""
+        self.SetRepetitions(n)
+
+    def PrintToScreen(self) -> None:
+        """CLTune PrintToScreen: one line per evaluated configuration, then the best."""
+        for r in self.rows():
+            t = f"{r.time_ms:10.4f} ms" if r.time_ms is not None else f"{r.status:>13s}"
+            print(f"[{r.step:6d}] {t}  {r.verified:8s}  {r.config}")
+        try:
+            cfg, ms = self.GetBestResult()
+            print(f"[ best ] {ms:10.4f} ms  {cfg}")
+        except K.KtcError:
+            print("[ best ] none (no successful configuration)")
+
+    def PrintToFile(self, path: str) -> None:
+        """CLTune PrintToFile: the results table as CSV (the reference's format)."""
+        self.write_csv(path)
+
     def write_csv(self, path: str) -> None:
         K.check(self._lib.ktc_tuner_write_csv(self._h, str(path).encode()))
 

@@ -125,3 +125,24 @@ def test_device_presets(built):
     assert abs(dm.peak_gflops - 148 * 128 * 2 * 1.965) < 1e-6
     with pytest.raises(K.KtcError):
         K.check(pkg.lib().ktc_device_preset(b"GTX9000", C.byref(dm)))
+
+
+def test_cltune_reporting_names(built, tmp_path, capsys):
+    """PrintToScreen / PrintToFile / SetNumRuns on a replayed search (no GPU)."""
+    table = tmp_path / "t.csv"
+    rows = ["config,time_ms"] + [f"WPT={w},1.{w}" for w in (1, 2, 4)]
+    table.write_text("\n".join(rows) + "\n")
+    t = pkg.Tuner(device=None, backend=f"replay:{table}")
+    t.SetDevice({"name": "tiny", "max_work_group_total": 256, "local_mem_bytes": 4096})
+    t.AddKernel("k.cu", "k", [64], [1])
+    t.AddParameter("WPT", [1, 2, 4])
+    t.DivGlobalSize(["WPT"])
+    t.AddArgumentOutput(64)
+    t.SetNumRuns(3)
+    t.UseFullSearch()
+    t.Tune()
+    t.PrintToScreen()
+    out = capsys.readouterr().out
+    assert "WPT=1" in out and "[ best ]" in out and "1.1000 ms" in out
+    t.PrintToFile(str(tmp_path / "r.csv"))
+    assert (tmp_path / "r.csv").read_text().count("\n") >= 4
