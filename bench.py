@@ -17,8 +17,9 @@ its output verified on the device against the bit-exact device reference.
   e2e    the same through the public API (Tuner, a fresh job per step):
          host materializes the inputs, H2D copy of the image and taps, D2H
          of the result rows -- all inside the timed region
-  tuned  per-filter best configuration (3..11, configs[1]) and the SGEMM
-         2048^3 winner (configs[2]) re-timed: GFLOPS, GB/s, roofline fraction
+  tuned  per-filter best configuration (3..11, configs[1]), the SGEMM
+         winners at 2048^3 / 4096^3 (configs[2], [4]) and the TF32 variant
+         re-timed: GFLOPS, GB/s, roofline fraction
   roofline  the best 3x3 convolution kernel (HBM-bound) against the measured
          copy bandwidth (MEASURED_PEAKS.json)
   cpu_baseline  the reference's own tuner loop (run_tuning + its synthetic
@@ -412,28 +413,26 @@ def tuned_block(pkg, local, threads, sample_best, peaks) -> dict:
             "frac": gbs / peaks["hbm_gbs"] if bound == "hbm" else gflops / fp32_peak,
             "dram_bytes": (entry or {}).get("dram_bytes"),
         }
-    g = table.get("gemm", {}).get("2048")
-    if g:
-        m = 2048
+    for size, g in sorted(table.get("gemm", {}).items(), key=lambda kv: int(kv[0])):
+        m = int(size)
         req = pkg.gemm_request(m, m, m, pkg.parse_canonical(g["config"]), reps=10)
         r = be.evaluate(req)
         req.repetitions = 30
         rs = sus.evaluate(req)
         if r.ok and rs.ok:
             gf = 2.0 * m ** 3 / (rs.mean_ms * 1e-3) / 1e9
-            out["sgemm_2048"] = {"config": g["config"], "time_ms": r.time_ms,
+            out[f"sgemm_{m}"] = {"config": g["config"], "time_ms": r.time_ms,
                                  "mean_ms": rs.mean_ms, "gflops": gf,
                                  "gflops_best": 2.0 * m ** 3 / (r.time_ms * 1e-3) / 1e9,
                                  "verified": r.verification, "bound": "fp32",
                                  "frac": gf / fp32_peak}
-    t = table.get("gemm_tf32", {}).get("2048")
-    if t:
-        m = 2048
+    for size, t in sorted(table.get("gemm_tf32", {}).items(), key=lambda kv: int(kv[0])):
+        m = int(size)
         r = be.evaluate(pkg.gemm_request(m, m, m, pkg.parse_canonical(t["config"]), reps=10,
                                          tf32=True))
         if r.ok:
             tf = 2.0 * m ** 3 / (r.time_ms * 1e-3) / 1e9
-            out["tf32_2048"] = {"config": t["config"], "time_ms": r.time_ms, "gflops": tf,
+            out[f"tf32_{m}"] = {"config": t["config"], "time_ms": r.time_ms, "gflops": tf,
                                 "verified": r.verification, "tolerance": "rel 1e-3, abs 1e-6"}
     out["fp32_peak_gflops"] = fp32_peak
     be.close()
