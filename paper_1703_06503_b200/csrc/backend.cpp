@@ -28,7 +28,7 @@
 
 #include "core.hpp"
 #include "ktb/arguments.hpp"
-#include "nvrtc_pool.hpp"
+#include "compile_service.hpp"
 
 namespace {
 

@@ -1,5 +1,5 @@
-// nvrtc_pool.cpp -- see nvrtc_pool.hpp.
-#include "nvrtc_pool.hpp"
+// compile_service.cpp -- see compile_service.hpp.
+#include "compile_service.hpp"
 
 #include <nvPTXCompiler.h>
 #include <nvrtc.h>

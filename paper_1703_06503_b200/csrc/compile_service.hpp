@@ -1,18 +1,21 @@
-// nvrtc_pool.hpp -- NVRTC compilation for sm_100a: a shared host thread pool,
-// batched programs and a cubin cache.
+// compile_service.hpp -- tuning-time compilation for sm_100a: a shared host
+// thread pool, cost-aware program formation and a cubin cache.
 //
 // Compilation is the throughput limiter of tuning (SURVEY 7 "Hard parts" 1).
-// Two levers:
+// Levers:
+//   * no NVVM for the built-in families: their KernelSource carries a PTX
+//     generator (ptxgen_conv.cpp / ptxgen_gemm.cpp) and programs go straight
+//     to ptxas (nvPTXCompiler, in process); NVRTC compiles the rest (TF32,
+//     custom kernels) from source;
 //   * ahead-of-time: callers prefetch() the configurations they will evaluate
 //     next, so the pool compiles while the device runs;
-//   * batching: up to `batch` configurations of the same family and problem
-//     are compiled as ONE NVRTC program (each configuration's kernel body in
-//     its own C++ namespace with its own macro block, entry names suffixed
-//     _k<i>).  NVRTC's fixed cost (~45 ms per program: front end, builtins)
-//     is paid once per batch.  A batch that fails to compile is split back
-//     into single compilations so errors land on the configuration that
-//     caused them.
-// Kernel sources carry a `//@@KTC_BODY@@` marker: the text above it (helpers,
+//   * program formation (take_program_locked): longest estimated compile
+//     first, then cheap configurations up to the thread's fair share of the
+//     queued cost and `batch` entries (each configuration its own entry
+//     _k<i>; in NVRTC sources, its own namespace and macro block).  A
+//     program that fails is split back into single compilations so errors
+//     land on the configuration that caused them.
+// NVRTC sources carry a `//@@KTC_BODY@@` marker: the text above it (helpers,
 // problem-level symbols) appears once per program, the text below it once per
 // configuration with KTC_ENTRY naming the kernel.
 #pragma once

@@ -27,7 +27,7 @@
 #include <string>
 #include <vector>
 
-#include "nvrtc_pool.hpp"
+#include "compile_service.hpp"
 
 namespace ktc {
 

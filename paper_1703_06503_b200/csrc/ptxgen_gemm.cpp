@@ -24,7 +24,7 @@
 #include <string>
 #include <vector>
 
-#include "nvrtc_pool.hpp"
+#include "compile_service.hpp"
 
 namespace ktc {
 

@@ -1,7 +1,7 @@
 """Where does the tuning-time NVRTC compile go?  (CPU only; no GPU needed.)
 
 Assembles the same batched program libktc builds for a batch of conv
-configurations (nvrtc_pool.cpp assemble(), backend.cpp plan_conv()) and
+configurations (compile_service.cpp assemble(), backend.cpp plan_conv()) and
 times nvrtcCompileProgram under option variants, optionally with NVRTC's
 --time phase breakdown.
 
