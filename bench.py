@@ -272,6 +272,13 @@ def main():
     order = list(range(valid))
     random.Random(2026).shuffle(order)  # fixed, seeded visit order for every N
 
+    # Every configuration of the run (warm-up, timed, e2e steps, all ranks)
+    # is distinct, so no compile is ever served from the cache inside a timed
+    # region: long runs shrink the per-step chunk instead of wrapping around.
+    total_steps = args.warmup + args.steps + max(1, min(2, args.steps))
+    if total_steps * world * args.chunk > valid:
+        args.chunk = max(1, valid // (total_steps * world))
+
     def units(step: int) -> list:
         base = (step * world + rank) * args.chunk
         return [order[(base + j) % valid] for j in range(args.chunk)]
