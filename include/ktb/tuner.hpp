@@ -118,5 +118,7 @@ std::optional<double> finish_row(const TuningJob& job, EvaluationResult& result,
 // RFC 4180 results CSV (CRLF), byte-compatible with write_results_csv.
 void write_results_csv(std::ostream& out, const TuningOutcome& outcome);
 std::string format_double(double v);
+// One RFC 4180 record (fields quoted when needed, CRLF), as every report uses.
+void write_csv_row(std::ostream& out, const std::vector<std::string>& fields);
 
 }  // namespace ktb

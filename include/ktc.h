@@ -396,6 +396,39 @@ int ktc_tuner_write_csv(ktc_tuner* t, const char* path);
 /* Replay table `config,time_ms` of the successful rows (backend.hpp:551-562). */
 int ktc_tuner_write_replay(ktc_tuner* t, const char* path);
 
+/* Repeated searches (`ktune stats`, tools/ktune.cpp:120-258): `runs` searches
+ * with seeds base_seed..base_seed+runs-1, spread as replicas over the tuner's
+ * devices (one whole search per device at a time).  Writes `out_csv` (best-of-
+ * run statistics + density, report.hpp:98-112), `<stem>_runs<ext>` (one row
+ * per run, report.hpp:87-96) and, for spaces of at most 100,000
+ * configurations, `<stem>_space<ext>` (the whole-space distribution from one
+ * full sweep sharded over every device).  Byte-identical to the reference's
+ * reports on the same per-configuration times. */
+typedef struct {
+    size_t runs;
+    double mean, stddev, min, max; /* best-of-run times (ms) */
+    int space_written;             /* 1 when <stem>_space was written */
+    size_t space_count;            /* successful rows in the full sweep */
+    double space_min, space_mean;
+    double wall_s;
+} ktc_stats_summary;
+int ktc_tuner_stats(ktc_tuner* t, size_t runs, uint64_t base_seed, const char* out_csv,
+                    ktc_stats_summary* out);
+
+/* What the CLI prints around a run (tools/ktune.cpp:84-117): the kernel and
+ * device names, the backend (its name() after Tune(), else the job's kind),
+ * the job's `output` path and the device ordinals the tuner will use. */
+typedef struct {
+    char kernel[128];
+    char device[128];
+    char backend[256];
+    char output[1024];
+    int is_cuda; /* 1 when the backend kind is "cuda" */
+    int ndevices;
+    int devices[64];
+} ktc_job_info;
+int ktc_tuner_job_info(ktc_tuner* t, ktc_job_info* out);
+
 /* Job files: the reference's JSON schema (jobfile.hpp) + backend kind
  * "cuda" ({"kind":"cuda","devices":[0],"flush_l2":true,...}). */
 int ktc_tuner_load_job(ktc_tuner* t, const char* json_text, const char* base_dir);

@@ -97,6 +97,7 @@ def ref_lib() -> C.CDLL:
         L.kr_job_price_table.argtypes = [C.c_char_p, C.c_char_p]
         L.kr_job_run.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_longlong),
                                  C.POINTER(C.c_double)]
+        L.kr_job_stats.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t, C.c_uint64, C.c_char_p]
         L.kr_job_throughput.argtypes = [C.c_char_p, C.c_int, C.c_size_t, C.POINTER(C.c_double),
                                         C.POINTER(C.c_double), C.POINTER(C.c_size_t)]
         _ref = L
@@ -217,6 +218,11 @@ def ref_job_run(job_json: str, base_dir: str, out_csv: str) -> tuple[int, float]
     _ref_check(ref_lib().kr_job_run(job_json.encode(), str(base_dir).encode(),
                                     str(out_csv).encode(), C.byref(bi), C.byref(bt)))
     return bi.value, bt.value
+
+
+def ref_job_stats(job_json: str, base_dir: str, runs: int, base_seed: int, out_csv: str) -> None:
+    _ref_check(ref_lib().kr_job_stats(job_json.encode(), str(base_dir).encode(), runs, base_seed,
+                                      str(out_csv).encode()))
 
 
 def ref_job_throughput(job_json: str, nthreads: int, per_thread: int) -> dict:

@@ -18,6 +18,11 @@
 //   kr_job_*            -> ktune::parse_job + compose_space + run_tuning
 //                          + write_results_csv         (jobfile.hpp:614,
 //                          tuner.hpp:181/194, report.hpp:62)
+//   kr_job_stats        -> the `ktune stats` sequence (tools/ktune.cpp:120-258:
+//                          run_tuning per seed, make_experiment_stats,
+//                          write_stats_csv / write_runs_csv); the CLI itself
+//                          needs CLI11, which is absent, so its body is
+//                          restated here over the same library calls
 #include <atomic>
 #include <chrono>
 #include <cstring>
@@ -28,6 +33,7 @@
 #include "ktune/jobfile.hpp"
 #include "ktune/landscapes.hpp"
 #include "ktune/report.hpp"
+#include "ktune/stats.hpp"
 #include "ktune/tuner.hpp"
 
 namespace {
@@ -209,6 +215,57 @@ int kr_job_run(const char* job_json, const char* base_dir, const char* out_csv,
         });
         *best_index = outcome.best_index ? static_cast<long long>(*outcome.best_index) : -1;
         *best_time_ms = outcome.best_time_ms ? *outcome.best_time_ms : 0.0;
+    });
+}
+
+// `ktune stats <job> --runs R --base-seed S --out <out_csv>`, serial
+// (tools/ktune.cpp:120-258).  Writes out_csv, <stem>_runs and, for spaces of
+// at most 100,000 configurations, <stem>_space.
+int kr_job_stats(const char* job_json, const char* base_dir, size_t runs, uint64_t base_seed,
+                 const char* out_csv) {
+    return guarded([&] {
+        ktune::LoadedJob loaded =
+            ktune::parse_job(std::string(job_json), std::filesystem::path(base_dir));
+        ktune::SearchSpace effective =
+            ktune::compose_space(loaded.job.kernel, loaded.job.device, loaded.job.space);
+        if (effective.valid_count() == 0) throw ktune::EmptySpaceAfterConstraints();
+        std::vector<ktune::RunSummary> summaries;
+        std::vector<double> bests;
+        for (size_t i = 0; i < runs; ++i) {
+            ktune::TuningJob job = loaded.job;
+            job.seed = base_seed + i;
+            ktune::TuningOutcome o = ktune::run_tuning(job, *loaded.backend, effective);
+            if (!o.best_time_ms) throw ktune::Error("run found no successful configuration");
+            summaries.push_back({i, job.seed, *o.best_time_ms, o.best_config->canonical()});
+            bests.push_back(*o.best_time_ms);
+        }
+        const std::filesystem::path out(out_csv);
+        auto derived = [&](const char* suffix) {
+            std::filesystem::path name = out.stem();
+            name += suffix;
+            name += out.extension();
+            return (out.parent_path() / name).string();
+        };
+        ktune::ExperimentStats stats = ktune::make_experiment_stats(bests);
+        ktune::save_report(out_csv, [&](std::ostream& o) { ktune::write_stats_csv(o, stats); });
+        ktune::save_report(derived("_runs"),
+                           [&](std::ostream& o) { ktune::write_runs_csv(o, summaries); });
+        if (effective.valid_count() <= 100000) {
+            ktune::TuningJob job = loaded.job;
+            job.strategy = ktune::StrategySpec{};
+            job.seed = base_seed;
+            ktune::TuningOutcome o = ktune::run_tuning(job, *loaded.backend, effective);
+            std::vector<double> times;
+            for (const ktune::TuningRow& row : o.rows)
+                if (row.status == ktune::Status::success &&
+                    row.verification != ktune::Verification::fail && row.time_ms)
+                    times.push_back(*row.time_ms);
+            if (!times.empty()) {
+                ktune::ExperimentStats space = ktune::make_experiment_stats(times);
+                ktune::save_report(derived("_space"),
+                                   [&](std::ostream& o) { ktune::write_stats_csv(o, space); });
+            }
+        }
     });
 }
 

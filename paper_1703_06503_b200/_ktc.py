@@ -128,6 +128,23 @@ class Summary(C.Structure):
     ]
 
 
+class StatsSummary(C.Structure):
+    _fields_ = [
+        ("runs", C.c_size_t), ("mean", C.c_double), ("stddev", C.c_double),
+        ("min", C.c_double), ("max", C.c_double), ("space_written", C.c_int),
+        ("space_count", C.c_size_t), ("space_min", C.c_double), ("space_mean", C.c_double),
+        ("wall_s", C.c_double),
+    ]
+
+
+class JobInfo(C.Structure):
+    _fields_ = [
+        ("kernel", C.c_char * 128), ("device", C.c_char * 128), ("backend", C.c_char * 256),
+        ("output", C.c_char * 1024), ("is_cuda", C.c_int), ("ndevices", C.c_int),
+        ("devices", C.c_int * 64),
+    ]
+
+
 # ---------------------------------------------------------------------------
 # library
 # ---------------------------------------------------------------------------
@@ -224,6 +241,8 @@ _SIGS = {
     "ktc_tuner_best": (C.c_int, [_P, C.c_char_p, C.c_size_t, C.POINTER(C.c_double)]),
     "ktc_tuner_write_csv": (C.c_int, [_P, C.c_char_p]),
     "ktc_tuner_write_replay": (C.c_int, [_P, C.c_char_p]),
+    "ktc_tuner_job_info": (C.c_int, [_P, C.POINTER(JobInfo)]),
+    "ktc_tuner_stats": (C.c_int, [_P, C.c_size_t, C.c_uint64, C.c_char_p, C.POINTER(StatsSummary)]),
     "ktc_tuner_load_job": (C.c_int, [_P, C.c_char_p, C.c_char_p]),
 }
 

@@ -12,6 +12,7 @@
 #include <sstream>
 
 #include "ktb/landscapes.hpp"
+#include "ktb/stats.hpp"
 #include "ktb/tuner.hpp"
 #include "ktc.h"
 
@@ -65,6 +66,17 @@ int guard(const std::function<void()>& fn) {
         ktc::set_error(e.what());
         return KTC_ERR_INVALID;
     }
+}
+
+// Reports are written in binary mode and checked after the flush
+// (report.hpp:114-127).
+template <class Write>
+void save_text(const std::string& path, Write&& write) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw Error("cannot open \"" + path + "\" for writing");
+    write(out);
+    out.flush();
+    if (!out) throw Error("failed while writing \"" + path + "\"");
 }
 
 void touched(ktc_tuner* t) {
@@ -912,6 +924,57 @@ int ktc_tuner_write_replay(ktc_tuner* t, const char* path) {
             if (r.status == Status::success && r.time_ms && r.verification != Verification::fail)
                 table.emplace(r.config.canonical(), *r.time_ms);
         ReplayBackend::save(path, table);
+    });
+}
+
+int ktc_tuner_stats(ktc_tuner* t, size_t runs, uint64_t base_seed, const char* out_csv,
+                    ktc_stats_summary* out) {
+    return guard([&] {
+        if (!out_csv) throw Error("ktc_tuner_stats: no output path");
+        const auto t0 = std::chrono::steady_clock::now();
+        ensure_backends(t);
+        if (t->ref_kernel && !t->ref_outputs) compute_reference_outputs(t);
+        std::vector<Backend*> bes;
+        for (auto& b : t->backends) bes.push_back(b.get());
+        StatsOutcome st = run_stats(t->job, bes, effective(t), runs, base_seed);
+        const std::string path(out_csv);
+        save_text(path, [&](std::ostream& o) { write_stats_csv(o, st.best_of_run); });
+        save_text(derive_report_path(path, "_runs"),
+                  [&](std::ostream& o) { write_runs_csv(o, st.runs); });
+        if (st.space)
+            save_text(derive_report_path(path, "_space"),
+                      [&](std::ostream& o) { write_stats_csv(o, *st.space); });
+        if (out) {
+            std::memset(out, 0, sizeof(*out));
+            const Summary& s = st.best_of_run.summary;
+            out->runs = s.count;
+            out->mean = s.mean;
+            out->stddev = s.stddev;
+            out->min = s.min;
+            out->max = s.max;
+            out->space_written = st.space ? 1 : 0;
+            if (st.space) {
+                out->space_count = st.space->summary.count;
+                out->space_min = st.space->summary.min;
+                out->space_mean = st.space->summary.mean;
+            }
+            out->wall_s =
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+    });
+}
+
+int ktc_tuner_job_info(ktc_tuner* t, ktc_job_info* out) {
+    return guard([&] {
+        std::memset(out, 0, sizeof(*out));
+        copy_str(t->job.kernel.name, out->kernel, sizeof(out->kernel));
+        copy_str(t->job.device.name, out->device, sizeof(out->device));
+        copy_str(t->outcome ? t->outcome->backend_name : t->backend_spec, out->backend,
+                 sizeof(out->backend));
+        copy_str(t->output, out->output, sizeof(out->output));
+        out->is_cuda = t->backend_spec == "cuda";
+        out->ndevices = int(std::min<size_t>(t->devices.size(), 64));
+        for (int i = 0; i < out->ndevices; ++i) out->devices[i] = t->devices[size_t(i)];
     });
 }
 

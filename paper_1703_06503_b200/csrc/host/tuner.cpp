@@ -399,6 +399,10 @@ std::string join_sizes(const std::vector<size_t>& s) {
 
 }  // namespace
 
+void write_csv_row(std::ostream& out, const std::vector<std::string>& fields) {
+    csv_row(out, fields);
+}
+
 void write_results_csv(std::ostream& out, const TuningOutcome& o) {
     csv_row(out, {"step", "config", "status", "time_ms", "global", "local", "best_so_far",
                   "verified"});

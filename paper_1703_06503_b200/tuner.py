@@ -291,6 +291,14 @@ class Tuner:
     def write_replay(self, path: str) -> None:
         K.check(self._lib.ktc_tuner_write_replay(self._h, str(path).encode()))
 
+    def Stats(self, runs: int, base_seed: int = 1, out: str = "stats.csv") -> dict:
+        """`ktune stats` (tools/ktune.cpp:120-258): `runs` searches with seeds
+        base_seed.., run as replicas over this tuner's devices; writes `out`,
+        `<stem>_runs<ext>` and (spaces <= 100,000) `<stem>_space<ext>`."""
+        s = K.StatsSummary()
+        K.check(self._lib.ktc_tuner_stats(self._h, runs, base_seed, str(out).encode(), C.byref(s)))
+        return {f: getattr(s, f) for f, _ in K.StatsSummary._fields_}
+
 
 def parse_canonical(text: str) -> dict:
     return {k: int(v) for k, v in (kv.split("=") for kv in text.split(";"))}
