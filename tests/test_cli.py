@@ -120,7 +120,9 @@ def test_cli_cuda_backend_tune_and_stats(tmp_path):
     assert "cuda" in p.stdout.splitlines()[0]
     job["strategy"] = {"kind": "annealing", "fraction": "1/256"}
     (tmp_path / "sa.json").write_text(json.dumps(job))
-    p = cli("stats", "sa.json", "--runs", 3, "--out", "s.csv", cwd=tmp_path)
+    # Two replicas sharing the one GPU of the test box (one per device in
+    # production: --gpus N).
+    p = cli("stats", "sa.json", "--runs", 3, "--out", "s.csv", "--devices", "0,0", cwd=tmp_path)
     assert p.returncode == 0, p.stderr
     runs = (tmp_path / "s_runs.csv").read_bytes().decode().split("\r\n")[1:-1]
     assert len(runs) == 3 and (tmp_path / "s_space.csv").exists()

@@ -71,3 +71,19 @@ def test_reference_external_backend_drives_b200_runner(built, tmp_path):
     assert len(rows) == 5104 // 512
     assert all(r[2] == "ok" and r[7] == "pass" for r in rows), rows
     assert bi >= 0 and bt > 0
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_measured_times_replay_through_reference_full_search(built, tmp_path):
+    """a full search measured on the B200 is saved as a replay
+    table and re-run through the reference's own run_full on its
+    ReplayBackend (backend.hpp:485-592): same best index, same best time."""
+    job = {"template": "conv", "problem": {"x": 1024, "y": 512, "filter": 5}, "device": B200,
+           "strategy": {"kind": "full"}, "verify": True, "repetitions": 2}
+    t = pkg.Tuner.from_job(json.dumps(dict(job, backend={"kind": "cuda"})), str(tmp_path))
+    s = t.Tune()
+    assert s["rows"] == 5104
+    t.write_replay(str(tmp_path / "measured.csv"))
+    rjob = dict(job, verify=False, backend={"kind": "replay", "path": "measured.csv"})
+    bi, bt = O.ref_job_run(json.dumps(rjob), str(tmp_path), str(tmp_path / "ref.csv"))
+    assert bi == s["best_index"] and bt == s["best_time_ms"]
