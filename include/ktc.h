@@ -415,6 +415,19 @@ typedef struct {
 int ktc_tuner_stats(ktc_tuner* t, size_t runs, uint64_t base_seed, const char* out_csv,
                     ktc_stats_summary* out);
 
+/* Report writers for replicas gathered across processes (one process per
+ * GPU): the best-of-run statistics (or a whole-space distribution) of
+ * `values` in the given order, and the per-run table -- the files
+ * ktc_tuner_stats writes (report.hpp:87-112). */
+typedef struct {
+    size_t run;
+    uint64_t seed;
+    double best_time_ms;
+    const char* best_config;
+} ktc_run_summary;
+int ktc_stats_write(const double* values, size_t n, const char* path);
+int ktc_runs_write(const ktc_run_summary* runs, size_t n, const char* path);
+
 /* What the CLI prints around a run (tools/ktune.cpp:84-117): the kernel and
  * device names, the backend (its name() after Tune(), else the job's kind),
  * the job's `output` path and the device ordinals the tuner will use. */

@@ -137,6 +137,11 @@ class StatsSummary(C.Structure):
     ]
 
 
+class RunSummary(C.Structure):
+    _fields_ = [("run", C.c_size_t), ("seed", C.c_uint64), ("best_time_ms", C.c_double),
+                ("best_config", C.c_char_p)]
+
+
 class JobInfo(C.Structure):
     _fields_ = [
         ("kernel", C.c_char * 128), ("device", C.c_char * 128), ("backend", C.c_char * 256),
@@ -241,6 +246,8 @@ _SIGS = {
     "ktc_tuner_best": (C.c_int, [_P, C.c_char_p, C.c_size_t, C.POINTER(C.c_double)]),
     "ktc_tuner_write_csv": (C.c_int, [_P, C.c_char_p]),
     "ktc_tuner_write_replay": (C.c_int, [_P, C.c_char_p]),
+    "ktc_stats_write": (C.c_int, [C.POINTER(C.c_double), C.c_size_t, C.c_char_p]),
+    "ktc_runs_write": (C.c_int, [C.POINTER(RunSummary), C.c_size_t, C.c_char_p]),
     "ktc_tuner_job_info": (C.c_int, [_P, C.POINTER(JobInfo)]),
     "ktc_tuner_stats": (C.c_int, [_P, C.c_size_t, C.c_uint64, C.c_char_p, C.POINTER(StatsSummary)]),
     "ktc_tuner_load_job": (C.c_int, [_P, C.c_char_p, C.c_char_p]),

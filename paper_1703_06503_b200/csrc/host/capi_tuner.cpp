@@ -964,6 +964,26 @@ int ktc_tuner_stats(ktc_tuner* t, size_t runs, uint64_t base_seed, const char* o
     });
 }
 
+int ktc_stats_write(const double* values, size_t n, const char* path) {
+    return guard([&] {
+        if (!path) throw Error("ktc_stats_write: no output path");
+        ExperimentStats st = make_experiment_stats(std::vector<double>(values, values + n));
+        save_text(path, [&](std::ostream& o) { write_stats_csv(o, st); });
+    });
+}
+
+int ktc_runs_write(const ktc_run_summary* runs, size_t n, const char* path) {
+    return guard([&] {
+        if (!path) throw Error("ktc_runs_write: no output path");
+        std::vector<RunSummary> rs;
+        rs.reserve(n);
+        for (size_t i = 0; i < n; ++i)
+            rs.push_back({runs[i].run, runs[i].seed, runs[i].best_time_ms,
+                          runs[i].best_config ? runs[i].best_config : ""});
+        save_text(path, [&](std::ostream& o) { write_runs_csv(o, rs); });
+    });
+}
+
 int ktc_tuner_job_info(ktc_tuner* t, ktc_job_info* out) {
     return guard([&] {
         std::memset(out, 0, sizeof(*out));

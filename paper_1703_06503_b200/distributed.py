@@ -64,3 +64,61 @@ def gather_merge(local_rows: list, world: int, group=None) -> MergedOutcome | No
     if dist.get_rank() != 0:
         return None
     return merge([r for part in everything for r in part])
+
+
+# ---------------------------------------------------------------------------
+# Repeated searches across processes (`ktune stats`, tools/ktune.cpp:120-258)
+# ---------------------------------------------------------------------------
+def stats_replicas(tuner, runs: int, base_seed: int, rank: int, world: int) -> list:
+    """Runs this rank's replicas -- run indices rank, rank+world, ... -- each a
+    whole search with seed base_seed + run on this rank's GPU (annealing and
+    PSO chains do not shard; K independent chains do).  Returns
+    (run, seed, best_time_ms, best_config) tuples."""
+    out = []
+    for run in range(rank, runs, world):
+        tuner.SetSeed(base_seed + run)
+        s = tuner.Tune()
+        if s["best_index"] < 0:
+            raise RuntimeError(f"run {run} (seed {base_seed + run}) found no successful "
+                               "configuration")
+        cfg, ms = tuner.GetBestResult()
+        out.append((run, base_seed + run, ms, cfg))
+    return out
+
+
+def write_stats_reports(runs: list, out_csv: str, space_times: list | None = None) -> None:
+    """rank 0: the reports ktc_tuner_stats writes, from gathered replicas --
+    `out_csv` (best-of-run statistics), `<stem>_runs<ext>` and, when the
+    whole-space times are given (unit order), `<stem>_space<ext>`."""
+    import ctypes as C
+    from pathlib import Path
+
+    from . import _ktc as K
+
+    lib = K.lib()
+    runs = sorted(runs)
+    vals = (C.c_double * len(runs))(*[r[2] for r in runs])
+    K.check(lib.ktc_stats_write(vals, len(runs), str(out_csv).encode()))
+    keep = [r[3].encode() for r in runs]
+    arr = (K.RunSummary * len(runs))(*[K.RunSummary(r[0], r[1], r[2], c)
+                                       for r, c in zip(runs, keep)])
+    p = Path(out_csv)
+    K.check(lib.ktc_runs_write(arr, len(runs), str(p.with_name(p.stem + "_runs" + p.suffix))
+                               .encode()))
+    if space_times:
+        st = (C.c_double * len(space_times))(*space_times)
+        K.check(lib.ktc_stats_write(st, len(space_times),
+                                    str(p.with_name(p.stem + "_space" + p.suffix)).encode()))
+
+
+def gather_runs(local: list, world: int, group=None) -> list | None:
+    """All ranks' replica tuples on rank 0 (None elsewhere)."""
+    if world == 1:
+        return list(local)
+    import torch.distributed as dist
+
+    everything = [None] * world if dist.get_rank() == 0 else None
+    dist.gather_object(local, everything, dst=0, group=group)
+    if dist.get_rank() != 0:
+        return None
+    return [r for part in everything for r in part]

@@ -8,6 +8,11 @@ summaries with the executor's rule (strict minimum, earliest index wins).
 
   python tools/gemm_full_search.py --size 2048 --start 0 --count 213152
   python tools/gemm_full_search.py --merge gpurun_out/gemm_full_*.json
+
+--dump-times writes every row's measured time (float32, enumeration order,
+NaN where a configuration failed or was not verified) to
+gpurun_out/gemm_full_<size>_<start>_times.npy -- a compact replay table for
+offline strategy studies (tools/gemm_strategy_study.py).
 """
 import argparse
 import json
@@ -19,7 +24,7 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 
-def run(size: int, start: int, count: int, prune: float) -> None:
+def run(size: int, start: int, count: int, prune: float, dump: bool = False) -> None:
     import paper_1703_06503_b200 as pkg
 
     t = pkg.Tuner.gemm(size, size, size)
@@ -45,6 +50,14 @@ def run(size: int, start: int, count: int, prune: float) -> None:
            "failures": [[r.space_index, r.status, r.verified, r.message[:120]]
                         for r in rows if not (r.status == "ok" and r.verified == "pass")][:20],
            "compile_s": s["compile_s"], "device_s": s["device_s"]}
+    (ROOT / "gpurun_out").mkdir(exist_ok=True)
+    if dump:
+        import numpy as np
+
+        times = np.full(stop - start, np.nan, dtype=np.float32)
+        for i, ms in ok:
+            times[i - start] = ms
+        np.save(ROOT / "gpurun_out" / f"gemm_full_{size}_{start:07d}_times.npy", times)
     out = ROOT / "gpurun_out" / f"gemm_full_{size}_{start:07d}.json"
     out.parent.mkdir(exist_ok=True)
     out.write_text(json.dumps(rec, indent=1))
@@ -76,8 +89,9 @@ if __name__ == "__main__":
     ap.add_argument("--count", type=int, default=213152)
     ap.add_argument("--prune", type=float, default=2.0)
     ap.add_argument("--merge", nargs="+")
+    ap.add_argument("--dump-times", action="store_true")
     a = ap.parse_args()
     if a.merge:
         merge(a.merge)
     else:
-        run(a.size, a.start, a.count, a.prune)
+        run(a.size, a.start, a.count, a.prune, a.dump_times)
