@@ -6,11 +6,13 @@
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out/replicas
 B=paper_1703_06503_b200/ktune-b200
-for j in gemm4096_pso6 gemm4096_sa4; do
-  /usr/bin/time -f "$j wall %e s" timeout 900 $B stats tools/jobs/$j.json --runs 8 --gpus 1 \
-      --out gpurun_out/replicas/$j.csv > gpurun_out/replicas/$j.log 2>&1; echo "$j rc=$?"
-  cat gpurun_out/replicas/$j.log | tail -4
-done
-/usr/bin/time -f "gemm8192_pso6 wall %e s" timeout 900 $B stats tools/jobs/gemm8192_pso6.json --runs 4 \
-    --gpus 1 --out gpurun_out/replicas/gemm8192_pso6.csv > gpurun_out/replicas/gemm8192_pso6.log 2>&1
-echo "gemm8192_pso6 rc=$?"; tail -4 gpurun_out/replicas/gemm8192_pso6.log
+run() {  # job runs
+  local t0=$SECONDS
+  timeout 900 $B stats tools/jobs/$1.json --runs $2 --gpus 1 --out gpurun_out/replicas/$1.csv \
+      > gpurun_out/replicas/$1.log 2>&1
+  echo "$1 rc=$? wall $((SECONDS - t0)) s" | tee -a gpurun_out/replicas/$1.log
+  tail -5 gpurun_out/replicas/$1.log
+}
+run gemm4096_pso6 8
+run gemm4096_sa4 8
+run gemm8192_pso6 4
