@@ -161,8 +161,21 @@ CubinPtr ptx_compile(const std::string& ptx) {
 }
 
 CompileService& CompileService::instance() {
-    static CompileService* svc = new CompileService;  // intentionally leaked: workers outlive statics
+    // Intentionally leaked (workers outlive statics); quiesced at exit.
+    static CompileService* svc = [] {
+        auto* s = new CompileService;
+        std::atexit([] { CompileService::instance().quiesce(); });
+        return s;
+    }();
     return *svc;
+}
+
+void CompileService::quiesce() {
+    std::unique_lock<std::mutex> lk(mu_);
+    exiting_ = true;
+    queues_.clear();
+    queued_cost_ = 0.0;
+    idle_cv_.wait_for(lk, std::chrono::seconds(60), [&] { return running_ == 0; });
 }
 
 void CompileService::configure(int threads, const std::string& cache_dir, int batch) {
@@ -371,14 +384,16 @@ void CompileService::worker() {
         double cost = 0.0;
         {
             std::unique_lock<std::mutex> lk(mu_);
-            cv_.wait(lk, [&] { return !queues_.empty(); });
+            cv_.wait(lk, [&] { return !queues_.empty() && !exiting_; });
             take_program_locked(&b);
             for (const Item& it : b.items) cost += it.cost;
             total_inflight_ += cost;
+            ++running_;
         }
         run_batch(std::move(b));
         std::lock_guard<std::mutex> lk(mu_);
         total_inflight_ -= cost;
+        if (--running_ == 0) idle_cv_.notify_all();
     }
 }
 

@@ -109,6 +109,11 @@ class CompileService {
     size_t programs_compiled();
     void reset_stats();
 
+    // Process exit (atexit): drops every queued (speculative) compile and
+    // waits for the programs already in ptxas/NVRTC to finish, so no worker
+    // is inside the compiler while static destructors run.
+    void quiesce();
+
   private:
     CompileService() = default;
     struct Item {
@@ -151,6 +156,9 @@ class CompileService {
     std::map<std::string, Queue> queues_;  // by batch key (source, problem)
     double queued_cost_ = 0.0;               // sum of queued item costs
     double total_inflight_ = 0.0;            // cost of programs being compiled
+    int running_ = 0;                        // batches inside run_batch
+    bool exiting_ = false;
+    std::condition_variable idle_cv_;
     std::unordered_map<std::string, std::shared_future<KernelPtr>> cache_;
     std::map<std::string, std::shared_ptr<const KernelSource>> sources_;
     std::vector<std::thread> workers_;

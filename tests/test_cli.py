@@ -126,3 +126,17 @@ def test_cli_cuda_backend_tune_and_stats(tmp_path):
     assert p.returncode == 0, p.stderr
     runs = (tmp_path / "s_runs.csv").read_bytes().decode().split("\r\n")[1:-1]
     assert len(runs) == 3 and (tmp_path / "s_space.csv").exists()
+
+
+@pytest.mark.gpu
+def test_cli_exits_cleanly_with_speculative_compiles_queued(tmp_path):
+    """Annealing prefetches every neighbour of the current GEMM configuration
+    into the compile pool; at exit the queued compiles are dropped and the
+    running ones drained before static destructors (was: free() abort)."""
+    job = {"template": "gemm", "problem": {"m": 1024, "n": 1024, "k": 1024}, "device": B200,
+           "backend": {"kind": "cuda"}, "verify": True,
+           "strategy": {"kind": "annealing", "fraction": "1/8192", "temperature": 4}}
+    (tmp_path / "sa.json").write_text(json.dumps(job))
+    p = cli("stats", "sa.json", "--runs", 2, "--out", "s.csv", cwd=tmp_path)
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert len((tmp_path / "s_runs.csv").read_bytes().decode().split("\r\n")) == 4
