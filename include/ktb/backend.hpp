@@ -66,6 +66,9 @@ class Backend {
     virtual size_t prefetch_depth() const { return 0; }
     // Device ordinal behind this backend, -1 if none.
     virtual int device() const { return -1; }
+    // A new search starts on this backend (drops per-search state such as
+    // the prune_factor bar).  Called by run_tuning / run_tuning_sharded.
+    virtual void begin_search() {}
     // CLTune SetReference: binds host reference outputs so the backend can
     // verify on its own (device-side).  Returns false when unsupported, in
     // which case the tuner verifies returned outputs on the host.
@@ -106,6 +109,7 @@ class CudaBackend : public Backend {
     size_t prefetch_depth() const override;
     std::string name() const override;
     int device() const override { return ordinal_; }
+    void begin_search() override { ktc_backend_begin_search(be_); }
     bool bind_reference(const EvaluationRequest& r, const std::vector<Buffer>& outputs) override;
     ktc_backend* handle() { return be_; }
     // Accounting of the last evaluate() and running totals.

@@ -90,9 +90,17 @@ TuningOutcome run_tuning(const TuningJob& job, Backend& backend);
 // of ReplayBackend) that already-evaluated successful configurations are
 // served from and new successful rows are appended to as they complete, so
 // an interrupted full search resumes where it stopped.
+//
+// The checkpoint is bound to the job that wrote it: `<path>.job` holds
+// job_signature(job) (kernel, source, argument recipes and problem scalars,
+// launch geometry, device, repetitions, verification rule).  Resuming with a
+// different job (e.g. GEMM 4096^3 on a 2048^3 checkpoint -- identical
+// configuration keys) throws instead of serving the other problem's times.
+std::string job_signature(const TuningJob& job);
+
 class ResultLog {
   public:
-    explicit ResultLog(const std::string& path);
+    explicit ResultLog(const std::string& path, const std::string& signature = "");
     bool lookup(const std::string& key, double* time_ms) const;
     void append(const std::string& key, double time_ms);
     size_t known() const { return table_.size(); }

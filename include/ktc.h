@@ -174,6 +174,10 @@ int ktc_verify_pair(ktc_ctx* ctx, ktc_buf cand, ktc_buf ref, size_t count, int e
  * and its 16-digit hex form (arguments.hpp:208-216). */
 uint64_t ktc_digest_words(const void* data, size_t n_words);
 void ktc_digest_hex(uint64_t digest, char out[17]);
+/* f32 `uniform:<seed>` recipe (arguments.hpp:126-180): out[i] =
+ * float(uniform01) of the i-th std::mt19937_64(seed) draw, bit-identical to
+ * the sequential stream, on up to `threads` host threads (jump-ahead). */
+int ktc_fill_uniform_f32(uint64_t seed, float* out, size_t n, int threads);
 
 /* ======================================================================= */
 /* 2. Evaluation backend: ktune::Backend::evaluate over the C ABI           */
@@ -263,6 +267,20 @@ int ktc_backend_prefetch(ktc_backend* be, const ktc_request* req);
 /* How many requests ahead a caller should keep prefetching so that every
  * NVRTC pool thread has work: 2 x pool threads x configurations per program. */
 size_t ktc_backend_prefetch_depth(ktc_backend* be);
+/* Starts a new search on this backend: forgets the prune_factor bar (the
+ * best verified time seen), so a search is never pruned against another
+ * search's (or another stats replica's) best. */
+int ktc_backend_begin_search(ktc_backend* be);
+/* Process-wide caches (measurement hygiene: a cold end-to-end run).
+ * KTC_DROP_COMPILED    the in-memory cubin cache of the compile pool (the
+ *                      next evaluation of any configuration compiles again;
+ *                      the optional on-disk cache is not touched)
+ * KTC_DROP_HOST_INPUTS the pinned host copies of materialized argument
+ *                      recipes (the next fresh job materializes its inputs
+ *                      on the host again) */
+#define KTC_DROP_COMPILED 1
+#define KTC_DROP_HOST_INPUTS 2
+int ktc_drop_caches(int flags);
 
 /* SetReference: binds host reference outputs (one buffer per output
  * argument, in order) for the argument list of `req`.  Built-in families

@@ -230,3 +230,22 @@ def ref_job_throughput(job_json: str, nthreads: int, per_thread: int) -> dict:
     _ref_check(ref_lib().kr_job_throughput(job_json.encode(), nthreads, per_thread,
                                            C.byref(rate), C.byref(wall), C.byref(n)))
     return {"configs_per_s": rate.value, "wall_s": wall.value, "evaluated": n.value}
+
+
+def ref_conv_apply(image, taps, x, y, f, w=1.0) -> np.ndarray:
+    """The reference's conv_apply (landscapes.hpp:120-143) as-is, one thread."""
+    out = np.empty(x * y, dtype=np.float32)
+    _ref_check(ref_lib().kr_conv_apply(np.ascontiguousarray(image, np.float32).ctypes.data,
+                                       np.ascontiguousarray(taps, np.float32).ctypes.data,
+                                       x, y, f, w, out.ctypes.data))
+    return out
+
+
+def ref_gemm_apply(a, b, c, m, n, k, alpha=1.0, beta=0.0) -> np.ndarray:
+    """The reference's gemm_apply (landscapes.hpp:293-312) as-is, one thread."""
+    out = np.empty(m * n, dtype=np.float32)
+    _ref_check(ref_lib().kr_gemm_apply(np.ascontiguousarray(a, np.float32).ctypes.data,
+                                       np.ascontiguousarray(b, np.float32).ctypes.data,
+                                       np.ascontiguousarray(c, np.float32).ctypes.data,
+                                       m, n, k, alpha, beta, out.ctypes.data))
+    return out

@@ -201,6 +201,9 @@ _SIGS = {
     "ktc_backend_evaluate": (C.c_int, [_P, C.POINTER(Request), C.POINTER(Result)]),
     "ktc_backend_prefetch": (C.c_int, [_P, C.POINTER(Request)]),
     "ktc_backend_prefetch_depth": (C.c_size_t, [_P]),
+    "ktc_backend_begin_search": (C.c_int, [_P]),
+    "ktc_drop_caches": (C.c_int, [C.c_int]),
+    "ktc_fill_uniform_f32": (C.c_int, [C.c_uint64, _P, C.c_size_t, C.c_int]),
     "ktc_backend_set_reference": (C.c_int, [_P, C.POINTER(Request), C.c_int, C.POINTER(_P),
                                             C.POINTER(C.c_size_t), C.POINTER(C.c_int)]),
     "ktc_backend_read_output": (C.c_int, [_P, C.c_int, _P, C.c_size_t]),
@@ -338,3 +341,15 @@ def device_count() -> int:
 
 
 os.environ.setdefault("KTC_LIB", str(LIB_PATH))
+
+
+DROP_COMPILED = 1
+DROP_HOST_INPUTS = 2
+
+
+def drop_caches(compiled: bool = True, host_inputs: bool = True) -> None:
+    """Forgets the process-wide compile (cubin) and pinned-input caches, so the
+    next fresh job compiles every configuration and materializes its inputs
+    on the host again (ktc_drop_caches)."""
+    check(lib().ktc_drop_caches((DROP_COMPILED if compiled else 0) |
+                                (DROP_HOST_INPUTS if host_inputs else 0)))

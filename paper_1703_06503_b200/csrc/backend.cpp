@@ -263,10 +263,21 @@ struct PinnedInput {
     }
 };
 
+struct RecipeCache {
+    std::mutex mu;
+    std::vector<std::pair<std::string, std::shared_ptr<PinnedInput>>> cache;
+    std::set<int> retained;  // devices whose primary context the cache keeps alive
+};
+RecipeCache& recipe_cache() {
+    static RecipeCache* rc = new RecipeCache;  // leaked: outlives static destructors
+    return *rc;
+}
+
 std::shared_ptr<PinnedInput> pinned_recipe(const ktb::ArgumentSpec& a, CUdevice dev) {
-    static std::mutex mu;
-    static std::vector<std::pair<std::string, std::shared_ptr<PinnedInput>>> cache;
-    static std::set<int> retained;  // devices whose primary context the cache keeps alive
+    RecipeCache& rc = recipe_cache();
+    std::mutex& mu = rc.mu;
+    auto& cache = rc.cache;
+    auto& retained = rc.retained;
     const std::string key = std::string(ktb::to_string(a.type)) + "|" + a.fill + "|" +
                             std::to_string(a.length);
     std::lock_guard<std::mutex> lk(mu);
@@ -1118,6 +1129,22 @@ int ktc_backend_prefetch(ktc_backend* be, const ktc_request* req) {
         set_error(e.what());
         return KTC_ERR_INVALID;
     }
+}
+
+int ktc_drop_caches(int flags) {
+    if (flags & KTC_DROP_COMPILED) CompileService::instance().drop_cache();
+    if (flags & KTC_DROP_HOST_INPUTS) {
+        RecipeCache& rc = recipe_cache();
+        std::lock_guard<std::mutex> lk(rc.mu);
+        rc.cache.clear();  // pinned blocks are freed when their last job releases them
+    }
+    return KTC_OK;
+}
+
+int ktc_backend_begin_search(ktc_backend* be) {
+    if (!be) return KTC_ERR_INVALID;
+    if (be->in) be->in->best_verified_ms = 0.0;
+    return KTC_OK;
 }
 
 size_t ktc_backend_prefetch_depth(ktc_backend* be) {

@@ -42,16 +42,21 @@ std::string hash_name(const std::string& key) {
 // (profiling runs: ncu source page); KTC_FAST_COMPILE=<0|min|mid|max>
 // selects NVRTC's --Ofast-compile level.  Both are part of the cache key.
 const std::vector<std::string>& base_options() {
-    static const std::vector<std::string> opts = [] {
-        std::vector<std::string> o = {"--gpu-architecture=sm_100a", "--std=c++17", "--fmad=true"};
+    // Leaked on purpose: pool workers may still read it while static
+    // destructors run (the atexit quiesce is registered before this static
+    // would be constructed, so a destructible vector would die first).
+    static const std::vector<std::string>* opts = [] {
+        auto* o_ = new std::vector<std::string>();
+        std::vector<std::string>& o = *o_;
+        o = {"--gpu-architecture=sm_100a", "--std=c++17", "--fmad=true"};
         const char* li = std::getenv("KTC_LINEINFO");
         if (li && std::strcmp(li, "0") != 0) o.push_back("-lineinfo");
         const char* fc = std::getenv("KTC_FAST_COMPILE");
         const std::string level = fc ? fc : kDefaultFastCompile;
         if (!level.empty() && level != "0") o.push_back("--Ofast-compile=" + level);
-        return o;
+        return o_;
     }();
-    return opts;
+    return *opts;
 }
 
 std::string define_name(const std::string& d) { return d.substr(0, d.find('=')); }
@@ -164,10 +169,21 @@ CompileService& CompileService::instance() {
     // Intentionally leaked (workers outlive statics); quiesced at exit.
     static CompileService* svc = [] {
         auto* s = new CompileService;
+        (void)base_options();  // construct before the quiesce handler is registered
         std::atexit([] { CompileService::instance().quiesce(); });
         return s;
     }();
     return *svc;
+}
+
+void CompileService::drop_cache() {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (auto it = cache_.begin(); it != cache_.end();) {
+        if (it->second.wait_for(std::chrono::seconds(0)) == std::future_status::ready)
+            it = cache_.erase(it);
+        else
+            ++it;
+    }
 }
 
 void CompileService::quiesce() {

@@ -108,6 +108,8 @@ class CompileService {
     double total_compile_ms();
     size_t programs_compiled();
     void reset_stats();
+    // Forgets every finished compile (in-memory cache); in-flight ones finish.
+    void drop_cache();
 
     // Process exit (atexit): drops every queued (speculative) compile and
     // waits for the programs already in ptxas/NVRTC to finish, so no worker

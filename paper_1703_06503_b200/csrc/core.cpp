@@ -1,5 +1,6 @@
 // core.cpp -- ktc.h layer 1: device primitives over the CUDA driver API.
 #include "core.hpp"
+#include "ktb/rng.hpp"
 
 #include <atomic>
 #include <chrono>
@@ -700,6 +701,17 @@ uint64_t ktc_digest_words(const void* data, size_t n_words) {
         h *= 0x100000001b3ull;
     }
     return h;
+}
+
+int ktc_fill_uniform_f32(uint64_t seed, float* out, size_t n, int threads) {
+    if (!out && n) return KTC_ERR_INVALID;
+    try {
+        ktb::fill_uniform_f32(seed, out, n, threads);
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return KTC_ERR_INVALID;
+    }
+    return KTC_OK;
 }
 
 void ktc_digest_hex(uint64_t digest, char out[17]) {

@@ -3,7 +3,9 @@
 #include <algorithm>
 #include <bit>
 #include <cstring>
+#include <cstdlib>
 #include <numeric>
+#include <thread>
 
 #include "ktb/arguments.hpp"
 #include "ktb/config.hpp"
@@ -69,6 +71,16 @@ FillRecipe parse_fill(const std::string& fill) {
     throw Error("malformed fill recipe \"" + fill + "\"");
 }
 
+// Host threads for large uniform recipes (KTC_MATERIALIZE_THREADS; default:
+// the hardware threads, at most 32).
+int materialize_threads() {
+    static const int n = [] {
+        if (const char* e = std::getenv("KTC_MATERIALIZE_THREADS")) return std::max(1, std::atoi(e));
+        return int(std::min(32u, std::max(1u, std::thread::hardware_concurrency())));
+    }();
+    return n;
+}
+
 void materialize_into(const ArgumentSpec& arg, void* out) {
     if (arg.role == ArgRole::scalar) throw Error("materialize_argument called on a scalar argument");
     const FillRecipe r = parse_fill(arg.fill);
@@ -81,11 +93,9 @@ void materialize_into(const ArgumentSpec& arg, void* out) {
             case FillRecipe::Kind::ramp:
                 for (size_t i = 0; i < n; ++i) d[i] = static_cast<float>(i);
                 break;
-            case FillRecipe::Kind::uniform: {
-                Rng rng(r.seed);
-                for (size_t i = 0; i < n; ++i) d[i] = static_cast<float>(uniform01(rng));
+            case FillRecipe::Kind::uniform:
+                fill_uniform_f32(r.seed, d, n, materialize_threads());
                 break;
-            }
         }
         return;
     }

@@ -579,7 +579,8 @@ void tune(ktc_tuner* t) {
         if (auto* c = dynamic_cast<CudaBackend*>(b)) c->reset_totals();
     auto t0 = std::chrono::steady_clock::now();
     std::unique_ptr<ResultLog> log;
-    if (!t->checkpoint.empty()) log = std::make_unique<ResultLog>(t->checkpoint);
+    if (!t->checkpoint.empty())
+        log = std::make_unique<ResultLog>(t->checkpoint, job_signature(t->job));
     TuningOutcome o = run_tuning_sharded(t->job, bes, eff, t->subset, log.get());
     ktc::trace_phase("tune: + search", tb);
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -7,7 +7,9 @@
 #include <cmath>
 #include <fstream>
 #include <mutex>
+#include <iterator>
 #include <ostream>
+#include <sstream>
 #include <thread>
 
 #include "ktb/landscapes.hpp"
@@ -170,6 +172,7 @@ std::optional<double> finish_row(const TuningJob& job, EvaluationResult& res, Tu
 
 TuningOutcome run_tuning(const TuningJob& job, Backend& backend, const SearchSpace& eff) {
     check_nonempty(job, eff);
+    backend.begin_search();
     TuningOutcome out;
     fill_header(out, job, backend, eff);
     std::vector<Buffer> reference;
@@ -237,10 +240,44 @@ TuningOutcome run_tuning(const TuningJob& job, Backend& backend) {
 // earliest wins, search.hpp:203-208).
 // ---------------------------------------------------------------------------
 
-ResultLog::ResultLog(const std::string& path) : path_(path) {
+std::string job_signature(const TuningJob& job) {
+    std::ostringstream s;
+    s.precision(17);
+    const KernelSpec& k = job.kernel;
+    s << "kernel=" << k.name << "\nsource=" << k.source_ref << "\nglobal=";
+    for (size_t g : k.base_global) s << g << ' ';
+    s << "\nlocal=";
+    for (size_t l : k.base_local) s << l << ' ';
+    s << "\nlocal_mem=" << k.local_mem_expr << "\nargs=";
+    for (const ArgumentSpec& a : k.arguments)
+        s << int(a.role) << ':' << int(a.type) << ':' << a.length << ':' << a.value << ':'
+          << a.fill << ' ';
+    s << "\ndevice=" << job.device.name << "\nrepetitions=" << job.repetitions
+      << "\nverify=" << job.verify << ' ' << job.rel_tol << ' ' << job.abs_tol << "\n";
+    return s.str();
+}
+
+ResultLog::ResultLog(const std::string& path, const std::string& signature) : path_(path) {
+    const std::string sig_path = path + ".job";
     std::ifstream probe(path, std::ios::binary);
-    if (probe) table_ = ReplayBackend::load(path).table();
-    else ReplayBackend::save(path, {});  // header only
+    if (probe) {
+        table_ = ReplayBackend::load(path).table();
+        if (!signature.empty() && !table_.empty()) {
+            std::ifstream sf(sig_path, std::ios::binary);
+            std::string recorded((std::istreambuf_iterator<char>(sf)),
+                                 std::istreambuf_iterator<char>());
+            if (recorded != signature)
+                throw Error("checkpoint " + path + " was written by a different job (" +
+                            (sf ? "signature mismatch in " + sig_path : "no " + sig_path) +
+                            "); refusing to resume from it");
+        }
+    } else {
+        ReplayBackend::save(path, {});  // header only
+    }
+    if (!signature.empty()) {
+        std::ofstream sf(sig_path, std::ios::binary | std::ios::trunc);
+        sf << signature;
+    }
 }
 
 bool ResultLog::lookup(const std::string& key, double* t) const {
@@ -266,7 +303,13 @@ TuningOutcome run_tuning_sharded(const TuningJob& job, const std::vector<Backend
     // Order-dependent strategies (annealing, PSO) are sequential chains: one
     // device, speculative compile-ahead of their candidate moves.
     if (!ordered) return run_tuning(job, *backends[0], eff);
+    // Above the enumeration limit there is no index table to shard: the
+    // sequential run_tuning samples by rejection (space.hpp sample_unique's
+    // large-space branch), as the reference does.
+    if (subset.empty() && eff.raw_size() > SearchSpace::kEnumerationLimit)
+        return run_tuning(job, *backends[0], eff);
     check_nonempty(job, eff);
+    for (Backend* b : backends) b->begin_search();
 
     TuningOutcome out;
     fill_header(out, job, *backends[0], eff);

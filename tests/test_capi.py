@@ -173,3 +173,23 @@ def test_gemm_ptx_codegen_matches_instruction_mix(built, tmp_path, row, dbuf):
     sg, sr = _sass(gen, tmp_path), _sass(ref, tmp_path)
     for op in ("FFMA2", "FFMA", "LDGSTS"):
         assert count(sg, op) == count(sr, op), op
+
+
+@pytest.mark.parametrize("n,seed", [(0, 1), (1000, 7), (4 * 2**20 - 1, 2026), (4 * 2**20, 2026),
+                                    (9 * 2**20 + 17, 12345),
+                                    (8194 * 4098, 2026),                      # configs[0] image
+                                    (2**22, 2026 ^ 0x9E3779B97F4A7C15)])       # GEMM B recipe
+def test_parallel_uniform_recipe_is_bit_identical(built, n, seed):
+    """ktc_fill_uniform_f32 (mt19937_64 jump-ahead over host threads) equals
+    the sequential reference stream (arguments.hpp:126-180) bit for bit."""
+    import ctypes as C
+
+    import numpy as np
+
+    from oracle import oracle as O
+
+    out = np.empty(max(1, n), np.float32)
+    for threads in (1, 3, 16):
+        assert pkg.lib().ktc_fill_uniform_f32(seed & (2**64 - 1), out.ctypes.data, n, threads) == 0
+        want = O.materialize(f"uniform:{seed}", n)
+        assert np.array_equal(out[:n].view(np.uint32), want.view(np.uint32)), threads

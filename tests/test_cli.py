@@ -140,3 +140,18 @@ def test_cli_exits_cleanly_with_speculative_compiles_queued(tmp_path):
     p = cli("stats", "sa.json", "--runs", 2, "--out", "s.csv", cwd=tmp_path)
     assert p.returncode == 0, p.stderr[-2000:]
     assert len((tmp_path / "s_runs.csv").read_bytes().decode().split("\r\n")) == 4
+
+
+@pytest.mark.gpu
+def test_cli_exits_cleanly_tf32_annealing(tmp_path):
+    """Same exit path for an NVRTC family (TF32): pool workers still inside
+    NVRTC at exit read the leaked option vector, never a destroyed static
+    (base_options() was destroyed before the quiesce handler ran)."""
+    job = {"template": "gemm_tf32", "problem": {"m": 1024, "n": 1024, "k": 1024}, "device": B200,
+           "backend": {"kind": "cuda"}, "verify": True,
+           "strategy": {"kind": "annealing", "fraction": "1/4", "temperature": 4}}
+    (tmp_path / "sa.json").write_text(json.dumps(job))
+    for _ in range(3):
+        p = cli("stats", "sa.json", "--runs", 2, "--out", "s.csv", cwd=tmp_path)
+        assert p.returncode == 0, p.stderr[-2000:]
+        assert len((tmp_path / "s_runs.csv").read_bytes().decode().split("\r\n")) == 4

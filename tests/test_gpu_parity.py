@@ -68,7 +68,7 @@ def test_device_reference_small_cases(backend, golden):
 
 
 # ------------------------------------------------------------- conv family
-@pytest.mark.parametrize("f", [3, 7, 11])
+@pytest.mark.parametrize("f", [3, 5, 7, 9, 11])
 def test_conv_configs_match_oracle(backend, f):
     x, y = 512, 256
     want = O.conv_reference(x, y, f)

@@ -196,3 +196,49 @@ def test_checkpoint_resume_reproduces_full_search(conv_table, tmp_path):
     again.write_csv(str(tmp_path / "mine.csv"))
     O.ref_job_run(text, str(conv_table), str(tmp_path / "ref.csv"))
     assert (tmp_path / "mine.csv").read_bytes() == (tmp_path / "ref.csv").read_bytes()
+
+
+def test_random_search_above_enumeration_limit_matches_reference(tmp_path):
+    """A custom space whose raw size (8 parameters x 8 values = 16.7M) is over
+    the enumeration limit: random search samples by rejection, exactly as the
+    reference's sample_unique does (space.hpp:443-460) -- same configurations,
+    same order (the sharded path used to refuse the space)."""
+    params = {f"P{i}": list(range(1, 9)) for i in range(8)}
+    job = {
+        "kernel": {"name": "copy", "source_ref": "copy.cu", "global": [4096], "local": [1],
+                   "arguments": [{"role": "output", "type": "f32", "length": 4096}]},
+        "space": {"parameters": params, "constraints": ["P0 + P1 != 3"]},
+        "device": {"name": "big", "max_work_group_total": 1024,
+                   "max_work_group_dim": [1024, 1024, 64], "local_mem_bytes": 49152},
+        "backend": {"kind": "replay", "path": "empty.csv"},
+        "strategy": {"kind": "random", "fraction": 1e-5},
+    }
+    (tmp_path / "empty.csv").write_text("config,time_ms\n")
+    ref, mine, _, t = run_both(tmp_path, job, devices=(0, 0))
+    assert mine == ref
+    assert len(t.rows()) > 100
+
+
+def test_checkpoint_refuses_a_different_job(conv_table, tmp_path):
+    """A checkpoint is bound to the job that wrote it: resuming a
+    different problem with the same configuration keys is an error, not a
+    silent reuse of the other problem's times."""
+    job = dict(CONV, backend={"kind": "replay", "path": "table.csv"}, strategy={"kind": "full"})
+    ckpt = tmp_path / "ckpt.csv"
+    first = pkg.Tuner.from_job(json.dumps(job), str(conv_table))
+    first.SetCheckpoint(str(ckpt))
+    first.SetSubset(list(range(50)))
+    first.Tune()
+    assert (tmp_path / "ckpt.csv.job").exists()
+    other = dict(job, problem={"filter": 5, "x": 4096})
+    t = pkg.Tuner.from_job(json.dumps(other), str(conv_table))
+    t.SetCheckpoint(str(ckpt))
+    t.SetSubset(list(range(50)))
+    with pytest.raises(Exception, match="different job"):
+        t.Tune()
+    # the same job resumes fine
+    again = pkg.Tuner.from_job(json.dumps(job), str(conv_table))
+    again.SetCheckpoint(str(ckpt))
+    again.SetSubset(list(range(50)))
+    again.Tune()
+    assert all(r.message == "resumed from checkpoint" for r in again.rows() if r.status == "ok")
