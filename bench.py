@@ -478,6 +478,21 @@ def main():
                         "peak_src": f"MEASURED_PEAKS.json hbm_gbs ({peaks['src']})"}
     if gemm_block:
         line["configs4_gemm4096"] = gemm_block
+    if rank == 0 and args.no_tuned:
+        # the roofline always uses the sustained protocol (30 back-to-back
+        # launches, mean): a single flushed launch can end before its output
+        # write-backs drain and read above the copy bandwidth
+        sus = pkg.CudaBackend(devices[0], compile_threads=threads, flush_l2=False, warmup=3)
+        req = pkg.conv_request(X, Y, F, pkg.parse_canonical(best_row.config), reps=30)
+        rs = sus.evaluate(req)
+        sus.close()
+        if rs.ok:
+            gbs = CONV_BYTES / (rs.mean_ms * 1e-3) / 1e9
+            line["roofline"].update(achieved=gbs, frac=gbs / peaks["hbm_gbs"],
+                                    kernel="conv2d_k0 " + best_row.config,
+                                    algorithmic_bytes=CONV_BYTES,
+                                    timing="mean of 30 back-to-back launches of this run's best "
+                                           "sampled configuration")
     if rank == 0 and not args.no_tuned:
         line["tuned"] = tuned_block(pkg, devices[0], threads, best_row, peaks)
         best3 = line["tuned"]["conv"].get("3")

@@ -348,7 +348,9 @@ int build_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
         // and every row start is 16-byte aligned for float4 / TMA.
         I.ipitch = int(round_up(round_up(size_t(I.X), 512) + I.F + 8, 64));
         I.rows = int(round_up(size_t(I.Y), 512) + I.F + 32);
+        const auto tm = Clock::now();
         std::shared_ptr<PinnedInput> img = pinned_recipe(I.args[4], ctx->dev);
+        trace_phase("inputs: image recipe (pinned)", tm);
         I.taps.resize(size_t(I.F) * I.F);
         ktb::materialize_into(I.args[5], I.taps.data());
         I.bytes[4] = size_t(I.ipitch) * I.rows * 4;
@@ -358,6 +360,7 @@ int build_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
         int st = ktc_upload_pitched(ctx, I.dev[4], size_t(I.ipitch) * 4, img->host, px * 4, px * 4,
                                     py);
         if (st) return st;
+        trace_phase("inputs: + H2D image", tm);
         I.bytes[5] = I.taps.size() * 4;
         CK(alloc(I.bytes[5], &I.dev[5]), "cuMemAlloc(taps)");
         CK(d.cuMemcpyHtoD(I.dev[5], I.taps.data(), I.bytes[5]), "cuMemcpyHtoD(taps)");

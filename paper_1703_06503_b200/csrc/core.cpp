@@ -67,6 +67,17 @@ CUresult launch(ktc_ctx* ctx, CUfunction fn, unsigned gx, unsigned gy, unsigned 
     return driver().cuLaunchKernel(fn, gx, gy, gz, bx, by, bz, smem, ctx->stream, params, nullptr);
 }
 
+// Longest a configuration's launches may run before it is declared hung
+// (runtime_error, context reset): KTC_WATCHDOG_S, default 30 s.
+double watchdog_seconds() {
+    static const double s = [] {
+        const char* e = std::getenv("KTC_WATCHDOG_S");
+        const double v = e ? std::atof(e) : 0.0;
+        return v > 0.0 ? v : 30.0;
+    }();
+    return s;
+}
+
 CUresult wait_event(ktc_ctx* ctx, CUevent ev, double timeout_s) {
     const Driver& d = driver();
     auto t0 = std::chrono::steady_clock::now();
@@ -617,7 +628,7 @@ int ktc_launch_timed(ktc_ctx* ctx, ktc_fn* fn, const unsigned grid[3], const uns
         if (rc == CUDA_SUCCESS) rc = d.cuEventRecord(ctx->events[2 * r + 1], ctx->stream);
         if (rc != CUDA_SUCCESS) return fail_cu(ctx, rc, "cuLaunchKernel");
     }
-    rc = wait_event(ctx, ctx->events[2 * reps - 1], 30.0);
+    rc = wait_event(ctx, ctx->events[2 * reps - 1], watchdog_seconds());
     if (rc != CUDA_SUCCESS) return fail_cu(ctx, rc, "kernel execution");
     float best = std::numeric_limits<float>::infinity();
     for (int r = 0; r < reps; ++r) {

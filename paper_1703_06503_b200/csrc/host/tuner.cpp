@@ -14,6 +14,10 @@
 
 #include "ktb/landscapes.hpp"
 
+namespace ktc {
+void trace_phase(const char* what, std::chrono::steady_clock::time_point since);
+}
+
 namespace ktb {
 
 std::string format_double(double v) {
@@ -327,6 +331,7 @@ TuningOutcome run_tuning_sharded(const TuningJob& job, const std::vector<Backend
     }
 
     const size_t n = units.size();
+    const auto t_start = std::chrono::steady_clock::now();
     std::vector<TuningRow> rows(n);
     std::vector<std::optional<double>> times(n);
     std::atomic<size_t> next{0}, prefetched{0};
@@ -367,6 +372,7 @@ TuningOutcome run_tuning_sharded(const TuningJob& job, const std::vector<Backend
                         continue;
                     }
                     EvaluationResult res = be.evaluate(req);
+                    if (i == 0) ktc::trace_phase("sharded: first unit", t_start);
                     times[i] = finish_row(job, res, row, &reference, &digests);
                     if (log && times[i]) log->append(row.config.canonical(), *times[i]);
                 }
@@ -379,6 +385,7 @@ TuningOutcome run_tuning_sharded(const TuningJob& job, const std::vector<Backend
     std::vector<std::thread> pool;
     for (size_t w = 0; w < backends.size(); ++w) pool.emplace_back(worker, w);
     for (auto& t : pool) t.join();
+    ktc::trace_phase("sharded: all units", t_start);
     for (const std::string& e : errors)
         if (!e.empty()) throw Error(e);
 
