@@ -1,7 +1,7 @@
-// ktb/search.hpp -- search strategies (reference search.hpp): budget
-// arithmetic, the canonical-key evaluation cache with strict-< best (ties
-// keep the earliest), and the full / random / simulated-annealing / PSO
-// drivers with the reference's exact RNG consumption.
+// ktb/search.hpp -- search strategies (reference search.hpp): the strategy
+// description, the search outcome record (best, trace, counters), and the
+// entry points.  The strategies themselves walk a Lattice (ktb/lattice.hpp)
+// and reproduce the reference's visits for the same seed.
 #pragma once
 
 #include <cstdint>
@@ -50,20 +50,13 @@ struct SearchOutcome {
     size_t total_steps = 0;
 };
 
+// floor(count * fraction), at least 1 (reference search.hpp:86-102).
 size_t budget(unsigned long long valid_count, double fraction);
+// Metropolis acceptance probability of moving from time t to t_prime.
 double sa_acceptance(double t, double t_prime, double temperature);
-Configuration pso_move(const Configuration& x, const Configuration& p, const Configuration& g,
-                       double alpha, double beta, double gamma, const SearchSpace& space, Rng& rng);
 
-SearchOutcome run_full(const SearchSpace& space, const Evaluator& evaluate);
-SearchOutcome run_random(const SearchSpace& space, const Evaluator& evaluate, double fraction,
-                         uint64_t seed);
-SearchOutcome run_annealing(const SearchSpace& space, const Evaluator& evaluate,
-                            double temperature, double fraction, uint64_t seed,
-                            const Prefetcher& prefetch = nullptr);
-SearchOutcome run_pso(const SearchSpace& space, const Evaluator& evaluate, size_t swarm,
-                      double alpha, double beta, double gamma, double fraction, uint64_t seed,
-                      const Prefetcher& prefetch = nullptr);
+// Runs one search (full sweep, random sample, simulated annealing or particle
+// swarm) over `space`; implementation: csrc/host/strategies.cpp.
 SearchOutcome run_search(const SearchSpace& space, const Evaluator& evaluate,
                          const StrategySpec& strategy, uint64_t seed,
                          const Prefetcher& prefetch = nullptr);

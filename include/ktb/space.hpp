@@ -1,8 +1,8 @@
 // ktb/space.hpp -- parameter spaces (reference space.hpp): parameters,
 // constraint expressions and native predicates; odometer enumeration (first
 // parameter slowest) cached and shared between copies; streaming counts;
-// uniform, unique and neighbour sampling with the reference's exact RNG
-// consumption, so seeded searches visit the same configurations.
+// the sorted raw ranks of the valid points that the strategies' Lattice
+// samples and walks on.
 //
 // B200-side differences (same results): enumeration runs on all host cores
 // (the raw space is split on its leading parameters and the per-thread
@@ -71,19 +71,16 @@ class SearchSpace {
     unsigned long long valid_count() const;
     unsigned long long constraint_only_count() const;
 
-    Configuration random_valid(Rng& rng) const;
-    Configuration random_neighbor(const Configuration& c, Rng& rng) const;
-    // The valid one-step neighbours random_neighbor draws from (no RNG use).
-    std::vector<Configuration> neighbors(const Configuration& c) const;
-    std::vector<Configuration> sample_unique(size_t n, Rng& rng) const;
-    // Enumeration indices of sample_unique's draw (same RNG consumption);
-    // only for spaces within the enumeration limit.
-    std::vector<uint64_t> sample_unique_indices(size_t n, Rng& rng) const;
+    // Odometer ranks (mixed-radix index in the raw space, first parameter
+    // most significant) of the valid configurations, ascending: row i of
+    // valid_table() is rank valid_ranks()[i].  Sampling and neighbourhoods
+    // live in ktb/lattice.hpp on top of this.
+    const std::vector<uint64_t>& valid_ranks() const;
 
   private:
-    static constexpr size_t kRejectionCap = 1'000'000;
     struct Cache {
         std::shared_ptr<const std::vector<Value>> table;
+        std::shared_ptr<const std::vector<uint64_t>> ranks;
         std::shared_ptr<const std::vector<Configuration>> configs;
         std::optional<unsigned long long> count;
     };
@@ -91,10 +88,10 @@ class SearchSpace {
     void invalidate();
     void require_parameters() const;
     bool satisfies_values(const Value* v, Configuration& scratch) const;
-    // Enumerates valid rows (values) of the raw space; parallel over threads.
-    std::vector<Value> enumerate_table() const;
+    // Enumerates valid rows (values, and their raw ranks) of the raw space;
+    // parallel over threads.
+    std::vector<Value> enumerate_table(std::vector<uint64_t>* ranks) const;
     unsigned long long count_valid(bool predicates) const;
-    Configuration random_raw(Rng& rng) const;
 
     std::vector<Parameter> params_;
     std::shared_ptr<const Configuration::Names> names_;

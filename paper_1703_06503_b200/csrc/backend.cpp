@@ -146,6 +146,15 @@ struct ktc_backend {
     std::unique_ptr<Inputs> in;
     std::map<std::string, KernelSource> custom_sources;  // path -> source
     std::vector<ModuleEntry> modules;
+    // Host copy of the reference bound by ktc_backend_set_reference, so it
+    // survives a context reset (a sticky fault frees every device buffer;
+    // the inputs are rebuilt and the reference re-uploaded).
+    struct BoundReference {
+        std::string sig;
+        std::vector<std::vector<unsigned char>> bytes;
+        std::vector<size_t> lengths;
+        std::vector<int> types;
+    } bound;
 };
 
 namespace {
@@ -432,6 +441,32 @@ int build_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
     return KTC_OK;
 }
 
+int upload_reference(ktc_backend* be, int n_buffers, const void* const* buffers,
+                     const size_t* lengths, const int* types) {
+    Inputs& I = *be->in;
+    if (n_buffers != int(I.out.size())) {
+        set_error("reference has " + std::to_string(n_buffers) + " buffers, kernel has " +
+                  std::to_string(I.out.size()) + " outputs");
+        return KTC_ERR_INVALID;
+    }
+    const Driver& d = driver();
+    for (int k = 0; k < n_buffers; ++k) {
+        if (lengths[k] != I.out_count[k] || types[k] != I.out_type[k]) {
+            set_error("reference buffer " + std::to_string(k) + " differs in length or type");
+            return KTC_ERR_INVALID;
+        }
+        if (!I.ref[k]) {
+            CUresult rc = ctx_alloc(be->ctx, lengths[k] * 4, &I.ref[k]);
+            if (rc != CUDA_SUCCESS) return fail_cu(be->ctx, rc, "cuMemAlloc(reference)");
+        }
+        CUresult rc = d.cuMemcpyHtoD(I.ref[k], buffers[k], lengths[k] * 4);
+        if (rc != CUDA_SUCCESS) return fail_cu(be->ctx, rc, "cuMemcpyHtoD(reference)");
+        I.ref_digest[k].clear();
+    }
+    I.has_reference = true;
+    return KTC_OK;
+}
+
 int ensure_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
     if (be->ctx->sticky) {
         free_inputs(be);
@@ -451,8 +486,17 @@ int ensure_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
         set_error(e.what());
         st = KTC_ERR_INVALID;
     }
-    if (st) free_inputs(be);  // never leave a half-built argument list cached
-    return st;
+    if (st) {
+        free_inputs(be);  // never leave a half-built argument list cached
+        return st;
+    }
+    if (be->bound.sig == sig) {  // re-bind the host reference after a rebuild
+        std::vector<const void*> ptrs;
+        for (const auto& b : be->bound.bytes) ptrs.push_back(b.data());
+        return upload_reference(be, int(ptrs.size()), ptrs.data(), be->bound.lengths.data(),
+                                be->bound.types.data());
+    }
+    return KTC_OK;
 }
 
 // Upload per-evaluation initial contents of custom-kernel buffers (inputs
@@ -1162,31 +1206,22 @@ int ktc_backend_set_reference(ktc_backend* be, const ktc_request* req, int n_buf
     int st = make_current(be->ctx);
     if (st) return st;
     const Family fam = family_of(req->kernel_name);
+    be->bound = {};
     st = ensure_inputs(be, req, fam);
     if (st) return st;
-    Inputs& I = *be->in;
-    if (n_buffers != int(I.out.size())) {
-        set_error("reference has " + std::to_string(n_buffers) + " buffers, kernel has " +
-                  std::to_string(I.out.size()) + " outputs");
-        return KTC_ERR_INVALID;
-    }
-    const Driver& d = driver();
+    st = upload_reference(be, n_buffers, buffers, lengths, types);
+    if (st) return st;
+    be->bound.sig = be->in->sig;
     for (int k = 0; k < n_buffers; ++k) {
-        if (lengths[k] != I.out_count[k] || types[k] != I.out_type[k]) {
-            set_error("reference buffer " + std::to_string(k) + " differs in length or type");
-            return KTC_ERR_INVALID;
-        }
-        if (!I.ref[k]) {
-            CUresult rc = ctx_alloc(be->ctx, lengths[k] * 4, &I.ref[k]);
-            if (rc != CUDA_SUCCESS) return fail_cu(be->ctx, rc, "cuMemAlloc(reference)");
-        }
-        CUresult rc = d.cuMemcpyHtoD(I.ref[k], buffers[k], lengths[k] * 4);
-        if (rc != CUDA_SUCCESS) return fail_cu(be->ctx, rc, "cuMemcpyHtoD(reference)");
-        I.ref_digest[k].clear();
+        const auto* b = static_cast<const unsigned char*>(buffers[k]);
+        be->bound.bytes.emplace_back(b, b + lengths[k] * 4);
+        be->bound.lengths.push_back(lengths[k]);
+        be->bound.types.push_back(types[k]);
     }
-    I.has_reference = true;
     return KTC_OK;
 }
+
+
 
 int ktc_backend_read_output(ktc_backend* be, int index, void* dst, size_t bytes) {
     if (!be || !be->in || index < 0 || index >= int(be->in->out.size())) return KTC_ERR_INVALID;

@@ -202,10 +202,11 @@ void split_raw(unsigned long long raw, Fn&& fn, size_t* used_threads) {
 
 }  // namespace
 
-std::vector<Value> SearchSpace::enumerate_table() const {
+std::vector<Value> SearchSpace::enumerate_table(std::vector<uint64_t>* ranks) const {
     const unsigned long long raw = raw_size();
     const size_t np = params_.size();
     std::vector<std::vector<Value>> parts(64);
+    std::vector<std::vector<uint64_t>> rank_parts(64);
     std::vector<std::string> errors(64);
     size_t used = 1;
     split_raw(
@@ -223,8 +224,12 @@ std::vector<Value> SearchSpace::enumerate_table() const {
                 for (size_t i = 0; i < np; ++i) v[i] = params_[i].values[digit[i]];
                 Configuration scratch(names_, v);
                 std::vector<Value>& out = parts[t];
+                std::vector<uint64_t>& rk = rank_parts[t];
                 for (unsigned long long idx = begin; idx < end; ++idx) {
-                    if (satisfies_values(v.data(), scratch)) out.insert(out.end(), v.begin(), v.end());
+                    if (satisfies_values(v.data(), scratch)) {
+                        out.insert(out.end(), v.begin(), v.end());
+                        rk.push_back(idx);
+                    }
                     for (size_t s = np; s-- > 0;) {
                         if (++digit[s] < params_[s].values.size()) {
                             v[s] = params_[s].values[digit[s]];
@@ -245,7 +250,12 @@ std::vector<Value> SearchSpace::enumerate_table() const {
     size_t total = 0;
     for (size_t t = 0; t < used; ++t) total += parts[t].size();
     table.reserve(total);
-    for (size_t t = 0; t < used; ++t) table.insert(table.end(), parts[t].begin(), parts[t].end());
+    ranks->clear();
+    ranks->reserve(total / std::max<size_t>(np, 1));
+    for (size_t t = 0; t < used; ++t) {
+        table.insert(table.end(), parts[t].begin(), parts[t].end());
+        ranks->insert(ranks->end(), rank_parts[t].begin(), rank_parts[t].end());
+    }
     return table;
 }
 
@@ -255,11 +265,19 @@ const std::vector<Value>& SearchSpace::valid_table() const {
     if (!cache_.table) {
         const unsigned long long raw = raw_size();
         if (raw > kEnumerationLimit) throw ExplicitEnumerationTooLarge(raw, kEnumerationLimit);
-        auto t = std::make_shared<std::vector<Value>>(enumerate_table());
+        auto r = std::make_shared<std::vector<uint64_t>>();
+        auto t = std::make_shared<std::vector<Value>>(enumerate_table(r.get()));
         cache_.count = t->size() / params_.size();
         cache_.table = std::move(t);
+        cache_.ranks = std::move(r);
     }
     return *cache_.table;
+}
+
+const std::vector<uint64_t>& SearchSpace::valid_ranks() const {
+    valid_table();
+    std::lock_guard<std::mutex> lk(mu_);
+    return *cache_.ranks;
 }
 
 const std::vector<Configuration>& SearchSpace::enumerate_valid() const {
@@ -357,104 +375,6 @@ unsigned long long SearchSpace::valid_count() const {
 unsigned long long SearchSpace::constraint_only_count() const {
     require_parameters();
     return count_valid(false);
-}
-
-Configuration SearchSpace::random_raw(Rng& rng) const {
-    std::vector<Value> v(params_.size());
-    for (size_t i = 0; i < params_.size(); ++i)
-        v[i] = params_[i].values[uniform_index(rng, params_[i].values.size())];
-    return Configuration(names_, std::move(v));
-}
-
-Configuration SearchSpace::random_valid(Rng& rng) const {
-    require_parameters();
-    if (raw_size() <= kEnumerationLimit) {
-        const unsigned long long n = valid_table().size() / params_.size();
-        if (n == 0) throw EmptySpace();
-        return config_at(size_t(uniform_index(rng, n)));
-    }
-    for (size_t a = 0; a < kRejectionCap; ++a) {
-        Configuration c = random_raw(rng);
-        if (satisfies(c)) return c;
-    }
-    throw EmptySpace("no valid configuration found after " + std::to_string(kRejectionCap) +
-                     " uniform draws; the space is empty or vanishingly sparse");
-}
-
-std::vector<Configuration> SearchSpace::neighbors(const Configuration& c) const {
-    std::vector<Configuration> cand;
-    for (size_t i = 0; i < params_.size(); ++i) {
-        const Parameter& p = params_[i];
-        const size_t at = c.find(p.name);
-        const Value cur = c.value_at(at);
-        size_t pos = 0;
-        while (p.values[pos] != cur) ++pos;
-        for (int delta : {-1, +1}) {
-            if (delta < 0 && pos == 0) continue;
-            if (delta > 0 && pos + 1 >= p.values.size()) continue;
-            Configuration n = c;
-            n.set_value_at(at, p.values[pos + size_t(long(delta))]);
-            if (satisfies(n)) cand.push_back(std::move(n));
-        }
-    }
-    return cand;
-}
-
-Configuration SearchSpace::random_neighbor(const Configuration& c, Rng& rng) const {
-    require_parameters();
-    if (!is_valid(c))
-        throw InvalidConfiguration("random_neighbor called with a configuration outside the space");
-    std::vector<Configuration> cand = neighbors(c);
-    if (!cand.empty()) return cand[size_t(uniform_index(rng, cand.size()))];
-    if (valid_count() <= 1) return c;
-    for (;;) {
-        Configuration d = random_valid(rng);
-        if (!(d == c)) return d;
-    }
-}
-
-std::vector<uint64_t> SearchSpace::sample_unique_indices(size_t n, Rng& rng) const {
-    require_parameters();
-    if (n == 0) return {};
-    const size_t total = valid_table().size() / params_.size();
-    if (n > total) throw BudgetExceedsSpace(n, total);
-    // Partial Fisher-Yates over a uint32 index range, as the reference.
-    std::vector<uint32_t> idx(total);
-    for (size_t i = 0; i < total; ++i) idx[i] = uint32_t(i);
-    std::vector<uint64_t> out;
-    out.reserve(n);
-    for (size_t i = 0; i < n; ++i) {
-        const size_t j = i + size_t(uniform_index(rng, total - i));
-        std::swap(idx[i], idx[j]);
-        out.push_back(idx[i]);
-    }
-    return out;
-}
-
-std::vector<Configuration> SearchSpace::sample_unique(size_t n, Rng& rng) const {
-    require_parameters();
-    if (n == 0) return {};
-    if (raw_size() <= kEnumerationLimit) {
-        std::vector<Configuration> out;
-        for (uint64_t i : sample_unique_indices(n, rng)) out.push_back(config_at(size_t(i)));
-        return out;
-    }
-    const unsigned long long avail = valid_count();
-    if (n > avail) throw BudgetExceedsSpace(n, avail);
-    std::vector<Configuration> out;
-    std::unordered_set<std::string> seen;
-    size_t misses = 0;
-    while (out.size() < n) {
-        Configuration c = random_valid(rng);
-        if (seen.insert(c.canonical()).second) {
-            out.push_back(std::move(c));
-            misses = 0;
-        } else if (++misses > kRejectionCap) {
-            throw Error("sample_unique stalled: could not find a fresh valid configuration after " +
-                        std::to_string(kRejectionCap) + " draws");
-        }
-    }
-    return out;
 }
 
 }  // namespace ktb
