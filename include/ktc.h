@@ -251,6 +251,14 @@ typedef struct {
      * configuration cannot become the best unless its best-of-N time is
      * below 1/prune_factor of its first flushed launch. */
     double prune_factor;
+    /* Process isolation (default 0): every call is forwarded to a persistent
+     * worker process per device (ktc-worker).  A configuration that faults
+     * (illegal address, trap: the CUDA context is lost for good) or hangs is
+     * a runtime_error row and the next evaluation gets a fresh worker, as
+     * the reference's external runner is isolated (external.hpp:278-286).
+     * The tuner turns it on for custom (user) kernels; KTC_ISOLATE=0/1
+     * overrides. */
+    int isolate;
 } ktc_backend_options;
 
 void ktc_backend_default_options(ktc_backend_options* opts);
@@ -281,6 +289,10 @@ int ktc_backend_begin_search(ktc_backend* be);
 #define KTC_DROP_COMPILED 1
 #define KTC_DROP_HOST_INPUTS 2
 int ktc_drop_caches(int flags);
+/* The isolated backend's worker loop (the ktc-worker executable is just
+ * this): serves one backend over framed requests on in_fd / out_fd until the
+ * parent closes it.  Not for direct use. */
+int ktc_worker_serve(int in_fd, int out_fd);
 
 /* SetReference: binds host reference outputs (one buffer per output
  * argument, in order) for the argument list of `req`.  Built-in families

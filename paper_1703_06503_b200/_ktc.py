@@ -96,7 +96,7 @@ class BackendOptions(C.Structure):
     _fields_ = [
         ("warmup", C.c_int), ("flush_l2", C.c_int), ("verify", C.c_int), ("rel_tol", C.c_double),
         ("abs_tol", C.c_double), ("compile_threads", C.c_int), ("cache_dir", C.c_char_p),
-        ("digest_outputs", C.c_int), ("prune_factor", C.c_double),
+        ("digest_outputs", C.c_int), ("prune_factor", C.c_double), ("isolate", C.c_int),
     ]
 
 
@@ -204,6 +204,7 @@ _SIGS = {
     "ktc_backend_begin_search": (C.c_int, [_P]),
     "ktc_drop_caches": (C.c_int, [C.c_int]),
     "ktc_fill_uniform_f32": (C.c_int, [C.c_uint64, _P, C.c_size_t, C.c_int]),
+    "ktc_worker_serve": (C.c_int, [C.c_int, C.c_int]),
     "ktc_backend_set_reference": (C.c_int, [_P, C.POINTER(Request), C.c_int, C.POINTER(_P),
                                             C.POINTER(C.c_size_t), C.POINTER(C.c_int)]),
     "ktc_backend_read_output": (C.c_int, [_P, C.c_int, _P, C.c_size_t]),

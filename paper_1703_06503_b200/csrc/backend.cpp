@@ -18,6 +18,8 @@
 #include <cstring>
 #include <fstream>
 #include <algorithm>
+#include <condition_variable>
+#include <thread>
 #include <map>
 #include <set>
 #include <memory>
@@ -27,6 +29,7 @@
 #include <vector>
 
 #include "core.hpp"
+#include "isolate.hpp"
 #include "ktb/arguments.hpp"
 #include "compile_service.hpp"
 
@@ -139,6 +142,7 @@ struct ModuleEntry {
 }  // namespace
 
 struct ktc_backend {
+    ktc::RemoteBackend* remote = nullptr;  // isolated: every call goes to a worker process
     ktc_ctx* ctx = nullptr;
     ktc_backend_options opts{};
     std::string name;
@@ -263,14 +267,115 @@ bool check_layout(const ktc_request* r, Family fam, std::string* why) {
 // that device's primary context (a job that closes the last backend must
 // not free them under the cache) and drops entries made before a
 // primary-context reset (primary_ctx_epoch).
+// Pinned blocks are pooled by exact size: dropping the recipe cache
+// (ktc_drop_caches) forgets the contents, not the page-locked allocations,
+// so a fresh job re-materializes into memory that is already pinned.
+struct PinnedPool {
+    std::mutex mu;
+    struct Block {
+        size_t bytes;
+        void* host;
+        unsigned epoch;
+    };
+    std::vector<Block> free;
+    size_t free_bytes = 0;
+    static constexpr size_t kCap = size_t(4) << 30;
+    void* take(size_t bytes, unsigned epoch) {
+        std::lock_guard<std::mutex> lk(mu);
+        for (size_t i = 0; i < free.size(); ++i)
+            if (free[i].bytes == bytes && free[i].epoch == epoch) {
+                void* p = free[i].host;
+                free_bytes -= bytes;
+                free.erase(free.begin() + long(i));
+                return p;
+            }
+        return nullptr;
+    }
+    void give(void* host, size_t bytes, unsigned epoch) {
+        std::lock_guard<std::mutex> lk(mu);
+        free.push_back({bytes, host, epoch});
+        free_bytes += bytes;
+        while (free_bytes > kCap && !free.empty()) {
+            if (free.front().epoch == primary_ctx_epoch()) driver().cuMemFreeHost(free.front().host);
+            free_bytes -= free.front().bytes;
+            free.erase(free.begin());
+        }
+    }
+};
+PinnedPool& pinned_pool() {
+    static PinnedPool* p = new PinnedPool;  // leaked: outlives static destructors
+    return *p;
+}
+
 struct PinnedInput {
     void* host = nullptr;
     size_t bytes = 0;
     unsigned epoch = 0;
     ~PinnedInput() {
-        if (host && epoch == primary_ctx_epoch()) driver().cuMemFreeHost(host);
+        if (host && epoch == primary_ctx_epoch()) pinned_pool().give(host, bytes ? bytes : 4, epoch);
     }
 };
+
+// Modules of a closed backend are unloaded off the caller's critical path
+// (cuModuleUnload can take milliseconds per module): one reaper thread per
+// process unloads them in the background.  Modules made before a context
+// reset died with it and are skipped.
+struct ModuleReaper {
+    std::mutex mu;
+    std::condition_variable cv;
+    struct Item {
+        CUcontext ctx;
+        CUmodule mod;
+        unsigned epoch;
+    };
+    std::vector<Item> queue;
+    bool started = false, busy = false, exiting = false;
+    std::condition_variable idle;
+    void retire(CUcontext ctx, CUmodule mod) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (exiting) return;  // the process is going away with its contexts
+        queue.push_back({ctx, mod, primary_ctx_epoch()});
+        if (!started) {
+            started = true;
+            std::thread([this] { run(); }).detach();
+        }
+        cv.notify_one();
+    }
+    void run() {
+        for (;;) {
+            std::vector<Item> batch;
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                busy = false;
+                idle.notify_all();
+                cv.wait(lk, [&] { return !queue.empty(); });
+                batch.swap(queue);
+                busy = true;
+            }
+            for (const Item& it : batch) {
+                if (it.epoch != primary_ctx_epoch()) continue;
+                driver().cuCtxSetCurrent(it.ctx);
+                driver().cuModuleUnload(it.mod);
+            }
+        }
+    }
+    // atexit: stop taking work and let an unload in progress finish, so no
+    // driver call is in flight while the process tears the driver down.
+    void quiesce() {
+        std::unique_lock<std::mutex> lk(mu);
+        exiting = true;
+        queue.clear();
+        idle.wait_for(lk, std::chrono::seconds(5), [&] { return !busy; });
+    }
+};
+ModuleReaper& module_reaper() {
+    static ModuleReaper* r = [] {
+        auto* m = new ModuleReaper;  // leaked: its thread outlives statics
+        std::atexit([] { module_reaper().quiesce(); });
+        return m;
+    }();
+    return *r;
+}
 
 struct RecipeCache {
     std::mutex mu;
@@ -303,8 +408,10 @@ std::shared_ptr<PinnedInput> pinned_recipe(const ktb::ArgumentSpec& a, CUdevice 
     auto p = std::make_shared<PinnedInput>();
     p->bytes = a.length * 4;
     p->epoch = epoch;
-    if (driver().cuMemHostAlloc(&p->host, p->bytes ? p->bytes : 4, CU_MEMHOSTALLOC_PORTABLE) !=
-        CUDA_SUCCESS) {
+    p->host = pinned_pool().take(p->bytes ? p->bytes : 4, epoch);
+    if (!p->host &&
+        driver().cuMemHostAlloc(&p->host, p->bytes ? p->bytes : 4, CU_MEMHOSTALLOC_PORTABLE) !=
+            CUDA_SUCCESS) {
         p->host = nullptr;
         throw ktb::Error("cuMemHostAlloc failed for a " + std::to_string(p->bytes) + "-byte input");
     }
@@ -1038,7 +1145,7 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
         out->kernel_launches = int(ctx->launches - launches0);
         // Sticky faults poison the context: reset now so the next
         // configuration starts clean (inputs are rebuilt lazily).
-        if (ctx->sticky) {
+        if (ctx->sticky && !ktc::g_isolated_worker) {
             be->modules.clear();  // modules died with the context
             free_inputs(be);
             int rs = ktc_reset(ctx);
@@ -1111,6 +1218,27 @@ void ktc_backend_default_options(ktc_backend_options* o) {
 
 int ktc_backend_open(int ordinal, const ktc_backend_options* opts, ktc_backend** out) {
     *out = nullptr;
+    bool isolate = opts && opts->isolate;
+    if (const char* e = std::getenv("KTC_ISOLATE")) isolate = std::atoi(e) != 0;
+    if (isolate && !ktc::g_isolated_worker) {
+        ktc_backend_options o;
+        if (opts) o = *opts;
+        else ktc_backend_default_options(&o);
+        std::string name, err;
+        ktc::RemoteBackend* rb =
+            ktc::remote_open(ordinal, o, o.cache_dir ? o.cache_dir : "", &name, &err);
+        if (!rb) {
+            set_error(err);
+            return KTC_ERR_CUDA;
+        }
+        auto* be = new ktc_backend;
+        be->remote = rb;
+        be->opts = o;
+        be->opts.cache_dir = nullptr;
+        be->name = name + " (isolated)";
+        *out = be;
+        return KTC_OK;
+    }
     ktc_ctx* ctx = nullptr;
     int st = ktc_open(ordinal, &ctx);
     if (st) return st;
@@ -1128,14 +1256,17 @@ int ktc_backend_open(int ordinal, const ktc_backend_options* opts, ktc_backend**
 
 void ktc_backend_close(ktc_backend* be) {
     if (!be) return;
+    if (be->remote) {
+        ktc::remote_close(be->remote);
+        delete be;
+        return;
+    }
     const auto t0 = std::chrono::steady_clock::now();
     free_inputs(be);
     trace_phase("close: free inputs", t0);
-    if (!be->ctx->sticky) {
-        driver().cuCtxSetCurrent(be->ctx->cu);
-        for (ModuleEntry& m : be->modules) driver().cuModuleUnload(m.mod);
-    }
-    trace_phase("close: + module unloads", t0);
+    if (!be->ctx->sticky)
+        for (ModuleEntry& m : be->modules) module_reaper().retire(be->ctx->cu, m.mod);
+    trace_phase("close: + module unloads (queued)", t0);
     be->modules.clear();
     ktc_close(be->ctx);
     trace_phase("close: + context", t0);
@@ -1143,10 +1274,11 @@ void ktc_backend_close(ktc_backend* be) {
 }
 
 const char* ktc_backend_name(ktc_backend* be) { return be ? be->name.c_str() : ""; }
-ktc_ctx* ktc_backend_ctx(ktc_backend* be) { return be ? be->ctx : nullptr; }
+ktc_ctx* ktc_backend_ctx(ktc_backend* be) { return be && !be->remote ? be->ctx : nullptr; }
 
 int ktc_backend_evaluate(ktc_backend* be, const ktc_request* req, ktc_result* out) {
     if (!be || !req || !out) return KTC_ERR_INVALID;
+    if (be->remote) return ktc::remote_evaluate(be->remote, req, out);
     try {
         return evaluate(be, req, out);
     } catch (const std::exception& e) {
@@ -1157,6 +1289,7 @@ int ktc_backend_evaluate(ktc_backend* be, const ktc_request* req, ktc_result* ou
 
 int ktc_backend_prefetch(ktc_backend* be, const ktc_request* req) {
     if (!be || !req) return KTC_ERR_INVALID;
+    if (be->remote) return ktc::remote_prefetch(be->remote, req);
     try {
         const Family fam = family_of(req->kernel_name);
         std::string why;
@@ -1179,6 +1312,7 @@ int ktc_backend_prefetch(ktc_backend* be, const ktc_request* req) {
 }
 
 int ktc_drop_caches(int flags) {
+    // (isolated backends: the worker processes keep their own caches)
     if (flags & KTC_DROP_COMPILED) CompileService::instance().drop_cache();
     if (flags & KTC_DROP_HOST_INPUTS) {
         RecipeCache& rc = recipe_cache();
@@ -1190,12 +1324,14 @@ int ktc_drop_caches(int flags) {
 
 int ktc_backend_begin_search(ktc_backend* be) {
     if (!be) return KTC_ERR_INVALID;
+    if (be->remote) return ktc::remote_begin_search(be->remote);
     if (be->in) be->in->best_verified_ms = 0.0;
     return KTC_OK;
 }
 
 size_t ktc_backend_prefetch_depth(ktc_backend* be) {
     if (!be) return 0;
+    if (be->remote) return ktc::remote_prefetch_depth(be->remote);
     CompileService& cs = CompileService::instance();
     return size_t(2) * size_t(cs.threads()) * size_t(cs.batch());
 }
@@ -1203,6 +1339,8 @@ size_t ktc_backend_prefetch_depth(ktc_backend* be) {
 int ktc_backend_set_reference(ktc_backend* be, const ktc_request* req, int n_buffers,
                               const void* const* buffers, const size_t* lengths, const int* types) {
     if (!be || !req) return KTC_ERR_INVALID;
+    if (be->remote)
+        return ktc::remote_set_reference(be->remote, req, n_buffers, buffers, lengths, types);
     int st = make_current(be->ctx);
     if (st) return st;
     const Family fam = family_of(req->kernel_name);
@@ -1224,6 +1362,7 @@ int ktc_backend_set_reference(ktc_backend* be, const ktc_request* req, int n_buf
 
 
 int ktc_backend_read_output(ktc_backend* be, int index, void* dst, size_t bytes) {
+    if (be && be->remote) return ktc::remote_read_output(be->remote, index, dst, bytes);
     if (!be || !be->in || index < 0 || index >= int(be->in->out.size())) return KTC_ERR_INVALID;
     size_t n = std::min(bytes, be->in->out_count[index] * 4);
     return ktc_download(be->ctx, dst, be->in->out[index], n);
@@ -1232,6 +1371,8 @@ int ktc_backend_read_output(ktc_backend* be, int index, void* dst, size_t bytes)
 int ktc_backend_read_reference(ktc_backend* be, const ktc_request* req, int index, void* dst,
                                size_t bytes, char digest_hex[17]) {
     if (!be || !req) return KTC_ERR_INVALID;
+    if (be->remote)
+        return ktc::remote_read_reference(be->remote, req, index, dst, bytes, digest_hex);
     int st = make_current(be->ctx);
     if (st) return st;
     st = ensure_inputs(be, req, family_of(req->kernel_name));

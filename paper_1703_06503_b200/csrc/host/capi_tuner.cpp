@@ -507,13 +507,18 @@ void ensure_backends(ktc_tuner* t) {
     for (int d : t->devices) key += ":" + std::to_string(d);
     key += "|" + std::to_string(t->opts.flush_l2) + std::to_string(t->opts.warmup) +
            std::to_string(t->opts.compile_threads) + std::to_string(t->job.rel_tol) +
-           std::to_string(t->job.abs_tol) + "|" + std::to_string(t->opts.prune_factor);
+           std::to_string(t->job.abs_tol) + "|" + std::to_string(t->opts.prune_factor) + "|" +
+           std::to_string(t->opts.isolate) + t->family;
     if (key == t->backends_key && !t->backends.empty()) return;
     t->backends.clear();
     if (t->backend_spec == "cuda") {
         ktc_backend_options o = t->opts;
         o.rel_tol = t->job.rel_tol;
         o.abs_tol = t->job.abs_tol;
+        // A user kernel may fault or hang; its evaluations run in a worker
+        // process per device so one bad configuration costs one row, not the
+        // process (the built-in families are generated and verified here).
+        if (t->family.empty()) o.isolate = 1;
         for (int d : t->devices) t->backends.push_back(std::make_unique<CudaBackend>(d, &o));
     } else if (t->backend_spec.rfind("replay:", 0) == 0) {
         // One replay worker per listed "device": exercises the sharded

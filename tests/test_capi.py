@@ -2,6 +2,7 @@
 point include/ktc.h declares, compiles both kernel families with NVRTC for
 sm_100a, and maps failures to codes instead of crashing."""
 import re
+import sys
 from pathlib import Path
 
 import pytest
@@ -193,3 +194,21 @@ def test_parallel_uniform_recipe_is_bit_identical(built, n, seed):
         assert pkg.lib().ktc_fill_uniform_f32(seed & (2**64 - 1), out.ctypes.data, n, threads) == 0
         want = O.materialize(f"uniform:{seed}", n)
         assert np.array_equal(out[:n].view(np.uint32), want.view(np.uint32)), threads
+
+
+def test_isolated_backend_worker_starts_and_reports_no_device(built):
+    """The isolated backend spawns ktc-worker; without a GPU the worker's
+    backend_open fails and the parent returns that error (no hang, no crash)."""
+    import subprocess
+
+    worker = Path(pkg.lib()._name).parent / "ktc-worker"
+    assert worker.exists()
+    if pkg.device_count() > 0:
+        pytest.skip("covered by the GPU fault tests")
+    code = ("import paper_1703_06503_b200 as p\n"
+            "try:\n    p.CudaBackend(0, isolate=True)\n    print('opened')\n"
+            "except p.KtcError as e:\n    print('error', e)\n")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120,
+                         cwd=str(Path(__file__).resolve().parent.parent))
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.startswith("error"), out.stdout

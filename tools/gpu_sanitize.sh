@@ -14,3 +14,7 @@ for tool in memcheck synccheck racecheck initcheck; do
       > gpurun_out/sanitizer/$tool.log 2>&1
   echo "$tool rc=$?"; tail -2 gpurun_out/sanitizer/$tool.log
 done
+# negative control: memcheck must flag the out-of-bounds write of a custom kernel
+timeout 600 $CS --tool memcheck --leak-check no --print-limit 5 python tools/sanitize_configs.py --control \
+    > gpurun_out/sanitizer/memcheck_control.log 2>&1
+echo "memcheck control rc=$? (expect errors reported)"; grep -m3 "Invalid\|ERROR SUMMARY" gpurun_out/sanitizer/memcheck_control.log

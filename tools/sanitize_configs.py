@@ -71,5 +71,40 @@ def main() -> int:
     return 1 if bad else 0
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--control" not in sys.argv:
     sys.exit(main())
+
+
+CONTROL = r"""
+extern "C" __global__ void oob(const int n, float* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i <= n) out[i] = 1.0f;   // i == n writes one element past the buffer
+}
+"""
+
+
+def control() -> int:
+    """Negative control: a custom kernel that writes one float past its
+    output buffer.  Under memcheck this run must report an invalid write
+    (proves the runtime-loaded cubins are instrumented)."""
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        src = Path(td) / "oob.cu"
+        src.write_text(CONTROL)
+        n = 1 << 20  # a whole number of blocks: out[n] lands right after the buffer
+        t = pkg.Tuner(devices=[0], flush_l2=False)
+        t.AddKernel(str(src), "oob", [n + 1], [1])
+        t.AddParameter("LS", [128])
+        t.MulLocalSize(["LS"])
+        t.AddArgumentScalar(n, "i32")
+        t.AddArgumentOutput(n, fill="constant:0")
+        t.UseFullSearch()
+        t.Tune()
+        for r in t.rows():
+            print("control row:", r.status, r.message[:160])
+    return 0
+
+
+if __name__ == "__main__" and "--control" in sys.argv:
+    sys.exit(control())
