@@ -55,7 +55,6 @@ class ConstraintExpr {
     };
 
   private:
-    friend class ConstraintParser;
     template <typename Fetch>
     Value run(Fetch&& fetch) const;
 

@@ -1,4 +1,13 @@
-// constraint.cpp -- parser and postfix evaluator of ktb::ConstraintExpr.
+// constraint.cpp -- the constraint language (grammar in ktb/constraint.hpp):
+// a scanner, a table-driven precedence parser that emits the postfix
+// program directly (no parse tree), and the evaluator.
+//
+// Parity with the reference (constraint.hpp:137-485): the whole text is
+// scanned before parsing, so a lexical error anywhere wins over a syntax
+// error; diagnostics carry the same messages and byte offsets; nesting is
+// refused with the same depth accounting (every precedence level and every
+// unary '!' or '(' descends one level; the check runs when an "or" level or
+// an operand is entered, against 256); comparisons do not chain.
 #include "ktb/constraint.hpp"
 
 #include <cctype>
@@ -8,296 +17,212 @@ namespace ktb {
 
 namespace {
 
-enum class Tok : uint8_t {
-    integer, identifier, lparen, rparen, bang, star, slash, percent, plus, minus,
-    lt, le, gt, ge, eq, ne, land, lor, end
-};
+using Op = ConstraintExpr::Op;
+using Insn = ConstraintExpr::Insn;
 
-struct Token {
-    Tok kind;
-    uint32_t begin, end;
+enum class Sym : uint8_t { number, name, open, close, bang, binop, end };
+
+struct Lexeme {
+    Sym sym;
+    Op op = Op::lit;  // binop: which operator
+    uint32_t begin = 0, end = 0;
     Value number = 0;
 };
 
-using Op = ConstraintExpr::Op;
-
-struct Node {
+struct Punct {
+    const char* text;
+    Sym sym;
     Op op;
-    Value lit = 0;
-    uint32_t param = 0;
-    int lhs = -1, rhs = -1;
-    uint32_t begin = 0, end = 0;
 };
 
+// Longest match first within each leading character.
+constexpr Punct kPuncts[] = {
+    {"||", Sym::binop, Op::or_jump}, {"&&", Sym::binop, Op::and_jump},
+    {"==", Sym::binop, Op::eq},      {"!=", Sym::binop, Op::ne},
+    {"<=", Sym::binop, Op::le},      {">=", Sym::binop, Op::ge},
+    {"<", Sym::binop, Op::lt},       {">", Sym::binop, Op::gt},
+    {"+", Sym::binop, Op::add},      {"-", Sym::binop, Op::sub},
+    {"*", Sym::binop, Op::mul},      {"/", Sym::binop, Op::div},
+    {"%", Sym::binop, Op::mod},      {"!", Sym::bang, Op::lnot},
+    {"(", Sym::open, Op::lit},       {")", Sym::close, Op::lit},
+};
+
+[[noreturn]] void syntax(const std::string& text, size_t off, const std::string& what) {
+    throw SyntaxError(text, off, what);
+}
+
+std::vector<Lexeme> scan(const std::string& s) {
+    std::vector<Lexeme> out;
+    size_t i = 0;
+    while (i < s.size()) {
+        const unsigned char c = static_cast<unsigned char>(s[i]);
+        const uint32_t b = uint32_t(i);
+        if (std::isspace(c)) {
+            ++i;
+        } else if (std::isdigit(c)) {
+            Value v = 0;
+            for (; i < s.size() && std::isdigit(static_cast<unsigned char>(s[i])); ++i) {
+                const int d = s[i] - '0';
+                if (v > (std::numeric_limits<Value>::max() - d) / 10)
+                    syntax(s, b, "integer literal too large");
+                v = v * 10 + d;
+            }
+            out.push_back({Sym::number, Op::lit, b, uint32_t(i), v});
+        } else if (std::isalpha(c) || c == '_') {
+            while (i < s.size() && (std::isalnum(static_cast<unsigned char>(s[i])) || s[i] == '_')) ++i;
+            out.push_back({Sym::name, Op::param, b, uint32_t(i), 0});
+        } else {
+            const Punct* hit = nullptr;
+            for (const Punct& p : kPuncts)
+                if (s.compare(i, std::char_traits<char>::length(p.text), p.text) == 0) {
+                    hit = &p;
+                    break;
+                }
+            if (!hit) {
+                // A lone '=', '&' or '|' names the operator it falls short of.
+                if (c == '=') syntax(s, b, "single '=' (use '==')");
+                if (c == '&') syntax(s, b, "single '&' (use '&&')");
+                if (c == '|') syntax(s, b, "single '|' (use '||')");
+                syntax(s, b, std::string("unexpected character '") + char(c) + "'");
+            }
+            i += std::char_traits<char>::length(hit->text);
+            out.push_back({hit->sym, hit->op, b, uint32_t(i), 0});
+        }
+    }
+    out.push_back({Sym::end, Op::lit, uint32_t(s.size()), uint32_t(s.size()), 0});
+    return out;
+}
+
+// Binary precedence levels, loosest first.  `chain`: left-associative
+// repetition; otherwise at most one operator at that level.
+struct Level {
+    Op ops[6];
+    int n;
+    bool chain;
+};
+constexpr Level kLevels[] = {
+    {{Op::or_jump}, 1, true},
+    {{Op::and_jump}, 1, true},
+    {{Op::eq, Op::ne, Op::le, Op::ge, Op::lt, Op::gt}, 6, false},
+    {{Op::add, Op::sub}, 2, true},
+    {{Op::mul, Op::div, Op::mod}, 3, true},
+};
+constexpr int kLevelCount = 5;
 constexpr int kMaxDepth = 256;
 
-}  // namespace
+bool at_level(int level, Op op) {
+    for (int k = 0; k < kLevels[level].n; ++k)
+        if (kLevels[level].ops[k] == op) return true;
+    return false;
+}
 
-// Recursive descent with the reference's depth accounting (each grammar
-// level adds one), so pathological nesting is refused at the same point.
-class ConstraintParser {
+struct Span {
+    uint32_t begin, end;
+};
+
+class Emitter {
   public:
-    ConstraintParser(const std::string& text, const Configuration::Names& names)
-        : text_(text), names_(names) {
-        tokenize();
-    }
+    Emitter(const std::string& text, const Configuration::Names& names, std::vector<Insn>& code,
+            std::vector<uint32_t>& params)
+        : text_(text), names_(names), code_(code), params_(params), lex_(scan(text)) {}
 
-    int run() {
-        int root = parse_or(0);
-        if (peek().kind != Tok::end) fail(peek().begin, "unexpected trailing input");
-        return root;
+    void run() {
+        level(0, 0);
+        if (lex_[at_].sym != Sym::end) syntax(text_, lex_[at_].begin, "unexpected trailing input");
     }
-
-    std::vector<Node> nodes;
 
   private:
-    [[noreturn]] void fail(size_t off, const std::string& what) const {
-        throw SyntaxError(text_, off, what);
+    void guard(int depth) const {
+        if (depth > kMaxDepth) syntax(text_, lex_[at_].begin, "expression nested too deeply");
     }
 
-    void push(Tok k, size_t b, size_t e, Value v = 0) {
-        toks_.push_back(Token{k, uint32_t(b), uint32_t(e), v});
+    void emit(Op op, Span s, uint32_t arg = 0, Value lit = 0) {
+        Insn in;
+        in.op = op;
+        in.arg = arg;
+        in.lit = lit;
+        in.begin = s.begin;
+        in.end = s.end;
+        code_.push_back(in);
     }
 
-    void tokenize() {
-        const std::string& s = text_;
-        size_t i = 0;
-        auto two = [&](char next) { return i + 1 < s.size() && s[i + 1] == next; };
-        while (i < s.size()) {
-            const unsigned char c = static_cast<unsigned char>(s[i]);
-            const size_t b = i;
-            if (std::isspace(c)) {
-                ++i;
-                continue;
+    // One precedence level at `depth`; its operands are the next level at
+    // depth + 1 (operands of the tightest level are primaries).
+    Span level(int lv, int depth) {
+        if (lv == 0) guard(depth);
+        if (lv == kLevelCount) return primary(depth);
+        Span lhs = level(lv + 1, depth + 1);
+        for (bool once = false; lex_[at_].sym == Sym::binop && at_level(lv, lex_[at_].op);) {
+            if (once && !kLevels[lv].chain) break;
+            once = true;
+            const Op op = lex_[at_++].op;
+            if (op == Op::and_jump || op == Op::or_jump) {
+                const size_t jump = code_.size();
+                emit(op, lhs);
+                const Span rhs = level(lv + 1, depth + 1);
+                lhs = {lhs.begin, rhs.end};
+                emit(Op::to_bool, lhs);
+                code_[jump].arg = uint32_t(code_.size());
+                code_[jump].end = lhs.end;
+            } else {
+                const Span rhs = level(lv + 1, depth + 1);
+                lhs = {lhs.begin, rhs.end};
+                emit(op, lhs);
             }
-            if (std::isdigit(c)) {
-                Value v = 0;
-                while (i < s.size() && std::isdigit(static_cast<unsigned char>(s[i]))) {
-                    const int dgt = s[i] - '0';
-                    if (v > (std::numeric_limits<Value>::max() - dgt) / 10)
-                        fail(b, "integer literal too large");
-                    v = v * 10 + dgt;
-                    ++i;
-                }
-                push(Tok::integer, b, i, v);
-                continue;
-            }
-            if (std::isalpha(c) || c == '_') {
-                while (i < s.size() &&
-                       (std::isalnum(static_cast<unsigned char>(s[i])) || s[i] == '_'))
-                    ++i;
-                push(Tok::identifier, b, i);
-                continue;
-            }
-            Tok k;
-            size_t len = 1;
-            switch (c) {
-                case '(': k = Tok::lparen; break;
-                case ')': k = Tok::rparen; break;
-                case '*': k = Tok::star; break;
-                case '/': k = Tok::slash; break;
-                case '%': k = Tok::percent; break;
-                case '+': k = Tok::plus; break;
-                case '-': k = Tok::minus; break;
-                case '!':
-                    if (two('=')) k = Tok::ne, len = 2;
-                    else k = Tok::bang;
-                    break;
-                case '<':
-                    if (two('=')) k = Tok::le, len = 2;
-                    else k = Tok::lt;
-                    break;
-                case '>':
-                    if (two('=')) k = Tok::ge, len = 2;
-                    else k = Tok::gt;
-                    break;
-                case '=':
-                    if (!two('=')) fail(b, "single '=' (use '==')");
-                    k = Tok::eq, len = 2;
-                    break;
-                case '&':
-                    if (!two('&')) fail(b, "single '&' (use '&&')");
-                    k = Tok::land, len = 2;
-                    break;
-                case '|':
-                    if (!two('|')) fail(b, "single '|' (use '||')");
-                    k = Tok::lor, len = 2;
-                    break;
-                default:
-                    fail(b, std::string("unexpected character '") + char(c) + "'");
-            }
-            i += len;
-            push(k, b, i);
         }
-        push(Tok::end, s.size(), s.size());
+        return lhs;
     }
 
-    const Token& peek() const { return toks_[pos_]; }
-    Token take() { return toks_[pos_++]; }
-    bool accept(Tok k) {
-        if (toks_[pos_].kind != k) return false;
-        ++pos_;
-        return true;
-    }
-    void depth_check(int d) const {
-        if (d > kMaxDepth) fail(peek().begin, "expression nested too deeply");
-    }
-
-    int add(Node n) {
-        nodes.push_back(n);
-        return int(nodes.size()) - 1;
-    }
-    int binary(Op op, int l, int r) {
-        Node n;
-        n.op = op;
-        n.lhs = l;
-        n.rhs = r;
-        n.begin = nodes[size_t(l)].begin;
-        n.end = nodes[size_t(r)].end;
-        return add(n);
-    }
-
-    int parse_or(int d) {
-        depth_check(d);
-        int l = parse_and(d + 1);
-        while (accept(Tok::lor)) l = binary(Op::or_jump, l, parse_and(d + 1));
-        return l;
-    }
-    int parse_and(int d) {
-        int l = parse_cmp(d + 1);
-        while (accept(Tok::land)) l = binary(Op::and_jump, l, parse_cmp(d + 1));
-        return l;
-    }
-    int parse_cmp(int d) {
-        int l = parse_sum(d + 1);
-        Op op;
-        switch (peek().kind) {
-            case Tok::eq: op = Op::eq; break;
-            case Tok::ne: op = Op::ne; break;
-            case Tok::le: op = Op::le; break;
-            case Tok::ge: op = Op::ge; break;
-            case Tok::lt: op = Op::lt; break;
-            case Tok::gt: op = Op::gt; break;
-            default: return l;
-        }
-        take();
-        return binary(op, l, parse_sum(d + 1));
-    }
-    int parse_sum(int d) {
-        int l = parse_term(d + 1);
-        for (;;) {
-            if (accept(Tok::plus)) l = binary(Op::add, l, parse_term(d + 1));
-            else if (accept(Tok::minus)) l = binary(Op::sub, l, parse_term(d + 1));
-            else return l;
-        }
-    }
-    int parse_term(int d) {
-        int l = parse_factor(d + 1);
-        for (;;) {
-            if (accept(Tok::star)) l = binary(Op::mul, l, parse_factor(d + 1));
-            else if (accept(Tok::slash)) l = binary(Op::div, l, parse_factor(d + 1));
-            else if (accept(Tok::percent)) l = binary(Op::mod, l, parse_factor(d + 1));
-            else return l;
-        }
-    }
-    int parse_factor(int d) {
-        depth_check(d);
-        const Token& t = peek();
-        switch (t.kind) {
-            case Tok::bang: {
-                Token bang = take();
-                int x = parse_factor(d + 1);
-                Node n;
-                n.op = Op::lnot;
-                n.lhs = x;
-                n.begin = bang.begin;
-                n.end = nodes[size_t(x)].end;
-                return add(n);
+    Span primary(int depth) {
+        guard(depth);
+        const Lexeme t = lex_[at_];
+        switch (t.sym) {
+            case Sym::bang: {
+                ++at_;
+                const Span x = primary(depth + 1);
+                const Span s{t.begin, x.end};
+                emit(Op::lnot, s);
+                return s;
             }
-            case Tok::lparen: {
-                Token open = take();
-                int inner = parse_or(d + 1);
-                if (!accept(Tok::rparen)) fail(peek().begin, "expected ')'");
-                nodes[size_t(inner)].begin = open.begin;  // diagnostics quote the parentheses
-                nodes[size_t(inner)].end = toks_[pos_ - 1].end;
-                return inner;
+            case Sym::open: {
+                ++at_;
+                level(0, depth + 1);
+                if (lex_[at_].sym != Sym::close) syntax(text_, lex_[at_].begin, "expected ')'");
+                // Diagnostics quote a parenthesized operand with its
+                // parentheses: widen the span of its root (the last insn).
+                const Span s{t.begin, lex_[at_++].end};
+                code_.back().begin = s.begin;
+                code_.back().end = s.end;
+                return s;
             }
-            case Tok::integer: {
-                Token lit = take();
-                Node n;
-                n.op = Op::lit;
-                n.lit = lit.number;
-                n.begin = lit.begin;
-                n.end = lit.end;
-                return add(n);
+            case Sym::number:
+                ++at_;
+                emit(Op::lit, {t.begin, t.end}, 0, t.number);
+                return {t.begin, t.end};
+            case Sym::name: {
+                ++at_;
+                const std::string name = text_.substr(t.begin, t.end - t.begin);
+                uint32_t slot = 0;
+                while (slot < names_.size() && names_[slot] != name) ++slot;
+                if (slot == names_.size()) throw UnknownParameter(name);
+                bool seen = false;
+                for (uint32_t q : params_) seen = seen || q == slot;
+                if (!seen) params_.push_back(slot);
+                emit(Op::param, {t.begin, t.end}, slot);
+                return {t.begin, t.end};
             }
-            case Tok::identifier: {
-                Token id = take();
-                const std::string name = text_.substr(id.begin, id.end - id.begin);
-                size_t idx = names_.size();
-                for (size_t i = 0; i < names_.size(); ++i)
-                    if (names_[i] == name) {
-                        idx = i;
-                        break;
-                    }
-                if (idx == names_.size()) throw UnknownParameter(name);
-                Node n;
-                n.op = Op::param;
-                n.param = uint32_t(idx);
-                n.begin = id.begin;
-                n.end = id.end;
-                return add(n);
-            }
-            case Tok::end: fail(t.begin, "unexpected end of input");
-            default: fail(t.begin, "expected a value, identifier, '!' or '('");
+            case Sym::end: syntax(text_, t.begin, "unexpected end of input");
+            default: syntax(text_, t.begin, "expected a value, identifier, '!' or '('");
         }
     }
 
     const std::string& text_;
     const Configuration::Names& names_;
-    std::vector<Token> toks_;
-    size_t pos_ = 0;
+    std::vector<Insn>& code_;
+    std::vector<uint32_t>& params_;
+    std::vector<Lexeme> lex_;
+    size_t at_ = 0;
 };
-
-namespace {
-
-void emit(const std::vector<Node>& nodes, int at, std::vector<ConstraintExpr::Insn>& code) {
-    const Node& n = nodes[size_t(at)];
-    ConstraintExpr::Insn in;
-    in.op = n.op;
-    in.begin = n.begin;
-    in.end = n.end;
-    switch (n.op) {
-        case Op::lit:
-            in.lit = n.lit;
-            code.push_back(in);
-            return;
-        case Op::param:
-            in.arg = n.param;
-            code.push_back(in);
-            return;
-        case Op::lnot:
-            emit(nodes, n.lhs, code);
-            code.push_back(in);
-            return;
-        case Op::and_jump:
-        case Op::or_jump: {
-            emit(nodes, n.lhs, code);
-            const size_t jump = code.size();
-            code.push_back(in);
-            emit(nodes, n.rhs, code);
-            ConstraintExpr::Insn b;
-            b.op = Op::to_bool;
-            code.push_back(b);
-            code[jump].arg = uint32_t(code.size());
-            return;
-        }
-        default:
-            emit(nodes, n.lhs, code);
-            emit(nodes, n.rhs, code);
-            code.push_back(in);
-    }
-}
 
 }  // namespace
 
@@ -307,27 +232,12 @@ ConstraintExpr ConstraintExpr::parse(std::string text,
     ConstraintExpr e;
     e.text_ = std::move(text);
     e.names_ = std::move(names);
-    ConstraintParser p(e.text_, *e.names_);
-    const int root = p.run();
-    emit(p.nodes, root, e.code_);
-    for (const Node& n : p.nodes) {
-        if (n.op != Op::param) continue;
-        bool seen = false;
-        for (uint32_t q : e.param_order_) seen = seen || q == n.param;
-        if (!seen) e.param_order_.push_back(n.param);
-    }
+    Emitter(e.text_, *e.names_, e.code_, e.param_order_).run();
     // Stack depth of the postfix program.
     int depth = 0, peak = 0;
     for (const Insn& in : e.code_) {
-        switch (in.op) {
-            case Op::lit:
-            case Op::param: ++depth; break;
-            case Op::lnot:
-            case Op::to_bool: break;
-            case Op::and_jump:
-            case Op::or_jump: --depth; break;  // the fall-through path pops
-            default: --depth; break;
-        }
+        if (in.op == Op::lit || in.op == Op::param) ++depth;
+        else if (in.op != Op::lnot && in.op != Op::to_bool) --depth;
         peak = std::max(peak, depth + 1);
     }
     e.max_stack_ = uint32_t(peak + 1);
