@@ -316,66 +316,6 @@ struct PinnedInput {
     }
 };
 
-// Modules of a closed backend are unloaded off the caller's critical path
-// (cuModuleUnload can take milliseconds per module): one reaper thread per
-// process unloads them in the background.  Modules made before a context
-// reset died with it and are skipped.
-struct ModuleReaper {
-    std::mutex mu;
-    std::condition_variable cv;
-    struct Item {
-        CUcontext ctx;
-        CUmodule mod;
-        unsigned epoch;
-    };
-    std::vector<Item> queue;
-    bool started = false, busy = false, exiting = false;
-    std::condition_variable idle;
-    void retire(CUcontext ctx, CUmodule mod) {
-        std::lock_guard<std::mutex> lk(mu);
-        if (exiting) return;  // the process is going away with its contexts
-        queue.push_back({ctx, mod, primary_ctx_epoch()});
-        if (!started) {
-            started = true;
-            std::thread([this] { run(); }).detach();
-        }
-        cv.notify_one();
-    }
-    void run() {
-        for (;;) {
-            std::vector<Item> batch;
-            {
-                std::unique_lock<std::mutex> lk(mu);
-                busy = false;
-                idle.notify_all();
-                cv.wait(lk, [&] { return !queue.empty(); });
-                batch.swap(queue);
-                busy = true;
-            }
-            for (const Item& it : batch) {
-                if (it.epoch != primary_ctx_epoch()) continue;
-                driver().cuCtxSetCurrent(it.ctx);
-                driver().cuModuleUnload(it.mod);
-            }
-        }
-    }
-    // atexit: stop taking work and let an unload in progress finish, so no
-    // driver call is in flight while the process tears the driver down.
-    void quiesce() {
-        std::unique_lock<std::mutex> lk(mu);
-        exiting = true;
-        queue.clear();
-        idle.wait_for(lk, std::chrono::seconds(5), [&] { return !busy; });
-    }
-};
-ModuleReaper& module_reaper() {
-    static ModuleReaper* r = [] {
-        auto* m = new ModuleReaper;  // leaked: its thread outlives statics
-        std::atexit([] { module_reaper().quiesce(); });
-        return m;
-    }();
-    return *r;
-}
 
 struct RecipeCache {
     std::mutex mu;
@@ -1264,9 +1204,13 @@ void ktc_backend_close(ktc_backend* be) {
     const auto t0 = std::chrono::steady_clock::now();
     free_inputs(be);
     trace_phase("close: free inputs", t0);
-    if (!be->ctx->sticky)
-        for (ModuleEntry& m : be->modules) module_reaper().retire(be->ctx->cu, m.mod);
-    trace_phase("close: + module unloads (queued)", t0);
+    if (!be->ctx->sticky) {
+        // Synchronous: a background unloader was measured to stall the next
+        // job's 134 MB H2D copy by up to 0.8 s (driver serialization).
+        driver().cuCtxSetCurrent(be->ctx->cu);
+        for (ModuleEntry& m : be->modules) driver().cuModuleUnload(m.mod);
+    }
+    trace_phase("close: + module unloads", t0);
     be->modules.clear();
     ktc_close(be->ctx);
     trace_phase("close: + context", t0);

@@ -1,7 +1,11 @@
 // backends.cpp -- ktb::ReplayBackend and ktb::CudaBackend.
+#include <cerrno>
 #include <charconv>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <iterator>
+#include <string_view>
 
 #include "ktb/backend.hpp"
 #include "ktb/tuner.hpp"
@@ -37,45 +41,59 @@ ReplayBackend ReplayBackend::load(const std::string& path) {
     return parse(in);
 }
 
+namespace {
+
+// One time field: the whole field must be a number (strtod syntax, as the
+// reference's std::stod), finite-range, then strictly positive.
+double replay_time(const std::string& field, size_t line) {
+    errno = 0;
+    char* end = nullptr;
+    const double t = field.empty() ? 0.0 : std::strtod(field.c_str(), &end);
+    if (field.empty() || end != field.c_str() + field.size() || errno == ERANGE)
+        throw MalformedReplayFile(line, "unparsable time \"" + field + "\"");
+    if (!(t > 0.0)) throw NonPositiveTime(t);
+    return t;
+}
+
+}  // namespace
+
 ReplayBackend ReplayBackend::parse(std::istream& in) {
+    // Whole file in memory, then one pass over its lines (LF or CRLF).
+    const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
     std::map<std::string, double> table;
-    std::string line;
-    size_t no = 0;
-    bool header = false;
-    while (std::getline(in, line)) {
-        ++no;
-        if (!line.empty() && line.back() == '\r') line.pop_back();
-        if (!header) {
-            if (line != "config,time_ms")
-                throw MalformedReplayFile(no, "expected header \"config,time_ms\"");
-            header = true;
+    size_t pos = 0, line = 0;
+    bool have_header = false;
+    while (pos < text.size()) {
+        size_t eol = text.find('\n', pos);
+        if (eol == std::string::npos) eol = text.size();
+        std::string_view row(text.data() + pos, eol - pos);
+        pos = eol + 1;
+        ++line;
+        if (!row.empty() && row.back() == '\r') row.remove_suffix(1);
+        if (!have_header) {
+            if (row != "config,time_ms")
+                throw MalformedReplayFile(line, "expected header \"config,time_ms\"");
+            have_header = true;
             continue;
         }
-        if (line.empty()) continue;
-        const size_t comma = line.find(',');
-        if (comma == std::string::npos || comma == 0)
-            throw MalformedReplayFile(no, "expected \"config,time_ms\"");
-        const std::string key = line.substr(0, comma), text = line.substr(comma + 1);
-        double t = 0.0;
-        try {
-            size_t used = 0;
-            t = std::stod(text, &used);
-            if (used != text.size()) throw std::invalid_argument("");
-        } catch (const std::exception&) {
-            throw MalformedReplayFile(no, "unparsable time \"" + text + "\"");
-        }
-        if (!(t > 0.0)) throw NonPositiveTime(t);
-        if (!table.emplace(key, t).second) throw MalformedReplayFile(no, "duplicate configuration key");
+        if (row.empty()) continue;
+        const size_t comma = row.find(',');
+        if (comma == std::string_view::npos || comma == 0)
+            throw MalformedReplayFile(line, "expected \"config,time_ms\"");
+        const double t = replay_time(std::string(row.substr(comma + 1)), line);
+        if (!table.try_emplace(std::string(row.substr(0, comma)), t).second)
+            throw MalformedReplayFile(line, "duplicate configuration key");
     }
-    if (!header) throw MalformedReplayFile(1, "empty file (missing header)");
+    if (!have_header) throw MalformedReplayFile(1, "empty file (missing header)");
     return ReplayBackend(std::move(table));
 }
 
 void ReplayBackend::save(const std::string& path, const std::map<std::string, double>& table) {
-    std::ofstream out(path, std::ios::binary);
-    if (!out) throw Error("cannot write replay file \"" + path + "\"");
-    out << "config,time_ms\n";
-    for (const auto& [k, t] : table) out << k << ',' << format_double(t) << '\n';
+    std::string out = "config,time_ms\n";
+    for (const auto& [key, t] : table) out.append(key).append(1, ',').append(format_double(t)).append(1, '\n');
+    std::ofstream f(path, std::ios::binary);
+    if (!f || !f.write(out.data(), std::streamsize(out.size())))
+        throw Error("cannot write replay file \"" + path + "\"");
 }
 
 EvaluationResult ReplayBackend::evaluate(const EvaluationRequest& r) {

@@ -242,3 +242,29 @@ def test_checkpoint_refuses_a_different_job(conv_table, tmp_path):
     again.SetSubset(list(range(50)))
     again.Tune()
     assert all(r.message == "resumed from checkpoint" for r in again.rows() if r.status == "ok")
+
+
+@pytest.mark.parametrize("body", [
+    "",                                             # empty file
+    "cfg,time\nA=1,2\n",                            # wrong header
+    "config,time_ms\r\nLOCAL=0,abc\r\n",            # unparsable time (CRLF)
+    "config,time_ms\nLOCAL=0,1e999\n",              # out of range
+    "config,time_ms\nLOCAL=0,-2.5\n",               # non-positive
+    "config,time_ms\nLOCAL=0,nan\n",                # NaN
+    "config,time_ms\nLOCAL=0,1.5\nLOCAL=0,2.5\n",   # duplicate key
+    "config,time_ms\n,1.5\n",                       # empty key
+    "config,time_ms\nLOCAL=0 1.5\n",                # no comma
+])
+def test_malformed_replay_tables_fail_like_the_reference(tmp_path, body):
+    (tmp_path / "t.csv").write_bytes(body.encode())
+    job = dict(CONV, backend={"kind": "replay", "path": "t.csv"},
+               strategy={"kind": "random", "fraction": "1/512"})
+    text = json.dumps(job)
+    with pytest.raises(Exception) as ref_err:
+        O.ref_job_run(text, str(tmp_path), str(tmp_path / "r.csv"))
+    with pytest.raises(Exception) as mine_err:
+        pkg.Tuner.from_job(text, str(tmp_path)).Tune()
+    # the reference's job loader prefixes "job file error: " (it loads the
+    # table while parsing the job); the diagnostic itself must be the same
+    want = str(ref_err.value).strip().removeprefix("job file error: ")
+    assert want in str(mine_err.value), (str(ref_err.value), str(mine_err.value))
