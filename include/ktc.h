@@ -244,12 +244,13 @@ typedef struct {
     const char* cache_dir;  /* on-disk cubin cache; NULL = memory only */
     int digest_outputs;     /* also FNV-digest outputs (D2H + host hash); default 0 */
     /* Early-out for device-bound searches; 0 (default) = off.  When > 0 and
-     * the first flushed timed launch of a configuration takes more than
-     * prune_factor x the best verified time this backend has seen for the
-     * same argument list, the remaining repetitions are skipped and that
-     * launch is the row's time (it is still verified).  Such a
-     * configuration cannot become the best unless its best-of-N time is
-     * below 1/prune_factor of its first flushed launch. */
+     * this backend has a verified best for the argument list, the warm-up
+     * launch of a configuration is flushed and timed (the probe); if it takes
+     * more than prune_factor x that best, the probe is the row's time and no
+     * further launches are made (the output is still verified).  Otherwise
+     * the repetitions follow as usual (the probe was their warm-up).  Such a
+     * configuration cannot become the best unless its best-of-N time is below
+     * 1/prune_factor of its first flushed launch. */
     double prune_factor;
     /* Process isolation (default 0): every call is forwarded to a persistent
      * worker process per device (ktc-worker).  A configuration that faults

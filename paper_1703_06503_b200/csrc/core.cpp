@@ -642,10 +642,10 @@ int ktc_launch_timed(ktc_ctx* ctx, ktc_fn* fn, const unsigned grid[3], const uns
     return KTC_OK;
 }
 
-// ktc_launch_timed with an early-out: when `bar` > 0 the first timed
-// repetition is waited for, and if it took longer than `bar` ms the rest are
-// skipped (*reps_done = 1).  Otherwise identical (same launches, flushes and
-// events).
+// ktc_launch_timed with an early-out: when `bar` > 0 the first warm-up
+// launch is flushed, timed and waited for (the probe); if it took longer
+// than `bar` ms that launch is the result (*reps_done = 1).  Otherwise the
+// timed repetitions follow with one warm-up fewer (the probe was one).
 int ktc_launch_timed_pruned(ktc_ctx* ctx, ktc_fn* fn, const unsigned grid[3],
                             const unsigned block[3], unsigned smem_bytes, void** params, int warmup,
                             int reps, int flush, double bar, float* best_ms, float* all_ms,
@@ -654,24 +654,21 @@ int ktc_launch_timed_pruned(ktc_ctx* ctx, ktc_fn* fn, const unsigned grid[3],
     if (!(bar > 0.0) || reps <= 1)
         return ktc_launch_timed(ctx, fn, grid, block, smem_bytes, params, warmup, reps, flush,
                                 best_ms, all_ms);
-    float first = 0.0f;
-    int st = ktc_launch_timed(ctx, fn, grid, block, smem_bytes, params, warmup, 1, flush, &first,
-                              all_ms);
+    // The warm-up launch doubles as the probe: flushed and timed like a
+    // repetition.  Over the bar, the configuration is done after one launch
+    // (its row time is that launch); otherwise the `reps` timed repetitions
+    // follow as usual and the probe only served as the warm-up.
+    float probe = 0.0f;
+    int st = ktc_launch_timed(ctx, fn, grid, block, smem_bytes, params, 0, 1, flush, &probe, nullptr);
     if (st) return st;
-    if (double(first) > bar) {
-        *best_ms = first;
+    if (double(probe) > bar) {
+        *best_ms = probe;
+        if (all_ms) all_ms[0] = probe;
         *reps_done = 1;
         return KTC_OK;
     }
-    std::vector<float> rest(size_t(reps - 1), 0.0f);
-    float best_rest = 0.0f;
-    st = ktc_launch_timed(ctx, fn, grid, block, smem_bytes, params, 0, reps - 1, flush, &best_rest,
-                          rest.data());
-    if (st) return st;
-    if (all_ms)
-        for (int r = 1; r < reps; ++r) all_ms[r] = rest[size_t(r - 1)];
-    *best_ms = std::min(first, best_rest);
-    return KTC_OK;
+    return ktc_launch_timed(ctx, fn, grid, block, smem_bytes, params, std::max(0, warmup - 1), reps,
+                            flush, best_ms, all_ms);
 }
 
 int ktc_bind_reference(ktc_ctx* ctx, ktc_buf ref, size_t count, int elem_type, double rel_tol,

@@ -24,10 +24,25 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 
-def run(size: int, start: int, count: int, prune: float, dump: bool = False) -> None:
+def run(size: int, start: int, count: int, prune: float, dump: bool = False,
+        checkpoint: str | None = None) -> None:
+    import shutil
+
     import paper_1703_06503_b200 as pkg
 
     t = pkg.Tuner.gemm(size, size, size)
+    if checkpoint:
+        # Resume file (replay CSV of verified rows): a shard cut off by the
+        # call's time limit continues where it stopped.  A copy travels in
+        # profiles/ (gpurun_out/ is not pushed to the box).
+        ck = ROOT / "gpurun_out" / Path(checkpoint).name
+        ck.parent.mkdir(exist_ok=True)
+        seed = ROOT / checkpoint
+        if seed.exists() and not ck.exists():
+            shutil.copy(seed, ck)
+            if Path(str(seed) + ".job").exists():
+                shutil.copy(str(seed) + ".job", str(ck) + ".job")
+        t.SetCheckpoint(str(ck))
     _, _, valid = t.space_counts()
     stop = min(valid, start + count)
     t.SetVerification(True)
@@ -90,8 +105,9 @@ if __name__ == "__main__":
     ap.add_argument("--prune", type=float, default=2.0)
     ap.add_argument("--merge", nargs="+")
     ap.add_argument("--dump-times", action="store_true")
+    ap.add_argument("--checkpoint", help="repo-relative seed checkpoint (copied to gpurun_out/)")
     a = ap.parse_args()
     if a.merge:
         merge(a.merge)
     else:
-        run(a.size, a.start, a.count, a.prune, a.dump_times)
+        run(a.size, a.start, a.count, a.prune, a.dump_times, a.checkpoint)
