@@ -6,7 +6,7 @@
 #include <cctype>
 #include <limits>
 #include <thread>
-#include <unordered_set>
+#include <unordered_map>
 
 namespace ktb {
 
@@ -46,22 +46,37 @@ static bool valid_identifier(const std::string& n) {
     return true;
 }
 
+namespace {
+
+// Value-list checks of add_parameter: the earliest offending position
+// decides which diagnostic is raised (a negative value, or a value listed
+// again later); at the same position the negative value is reported.
+void check_values(const std::string& name, const std::vector<Value>& values) {
+    if (values.empty()) throw EmptyValueList(name);
+    constexpr size_t none = static_cast<size_t>(-1);
+    size_t negative = none, repeated = none;
+    std::unordered_map<Value, size_t> first;  // value -> first position
+    for (size_t i = 0; i < values.size(); ++i) {
+        if (values[i] < 0 && negative == none) negative = i;
+        auto [it, fresh] = first.try_emplace(values[i], i);
+        if (!fresh) repeated = std::min(repeated, it->second);
+    }
+    if (negative != none && negative <= repeated)
+        throw Error("parameter \"" + name + "\" has a negative value " +
+                    std::to_string(values[negative]));
+    if (repeated != none)
+        throw Error("parameter \"" + name + "\" lists value " + std::to_string(values[repeated]) +
+                    " twice");
+}
+
+}  // namespace
+
 SearchSpace& SearchSpace::add_parameter(std::string name, std::vector<Value> values,
                                         std::vector<std::string> labels) {
     if (!valid_identifier(name))
         throw Error("parameter name \"" + name + "\" must match [A-Za-z_][A-Za-z0-9_]*");
-    for (const Parameter& p : params_)
-        if (p.name == name) throw DuplicateParameter(name);
-    if (values.empty()) throw EmptyValueList(name);
-    for (size_t i = 0; i < values.size(); ++i) {
-        if (values[i] < 0)
-            throw Error("parameter \"" + name + "\" has a negative value " +
-                        std::to_string(values[i]));
-        for (size_t j = i + 1; j < values.size(); ++j)
-            if (values[i] == values[j])
-                throw Error("parameter \"" + name + "\" lists value " + std::to_string(values[i]) +
-                            " twice");
-    }
+    if (has_parameter(name)) throw DuplicateParameter(name);
+    check_values(name, values);
     if (!labels.empty() && labels.size() != values.size())
         throw Error("parameter \"" + name + "\" has " + std::to_string(labels.size()) +
                     " labels for " + std::to_string(values.size()) + " values");

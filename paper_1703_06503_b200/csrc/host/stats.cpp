@@ -1,7 +1,8 @@
 // Repeated-search statistics (reference: include/ktune/stats.hpp,
-// report.hpp:80-112, tools/ktune.cpp:120-258).  The arithmetic follows the
-// reference operation for operation (same summation orders, same grid, same
-// renormalization) so the reports are byte-identical on the same samples.
+// report.hpp:80-112, tools/ktune.cpp:120-258): per-run summaries gathered
+// from replicas, the sample moments and a Gaussian density of the best
+// times, and the report writers.  The floating-point evaluation order is
+// dictated by byte-parity of the reports with the reference's.
 #include "ktb/stats.hpp"
 
 #include <algorithm>
@@ -15,77 +16,91 @@
 
 namespace ktb {
 
-Summary summarize(const std::vector<double>& values) {
-    if (values.empty()) throw Error("cannot summarize an empty sample");
-    Summary s;
-    s.count = values.size();
-    s.min = s.max = values.front();
-    double sum = 0.0;
-    for (double v : values) {
-        sum += v;
-        s.min = std::min(s.min, v);
-        s.max = std::max(s.max, v);
-    }
-    s.mean = sum / double(values.size());
-    if (values.size() > 1) {
-        double sq = 0.0;
-        for (double v : values) sq += (v - s.mean) * (v - s.mean);
-        s.stddev = std::sqrt(sq / double(values.size() - 1));
-    }
-    return s;
-}
-
 namespace {
 
-// Type-7 (linear interpolation) quantile of a sorted sample.
-double quantile7(const std::vector<double>& sorted, double p) {
-    const double pos = p * double(sorted.size() - 1);
-    const size_t lo = size_t(pos);
-    const size_t hi = std::min(lo + 1, sorted.size() - 1);
-    const double w = pos - double(lo);
-    return sorted[lo] * (1.0 - w) + sorted[hi] * w;
+// Moments of a sample in one object: the running sum and extremes in sample
+// order, then the (n-1) deviation around the mean.  Floating-point order is
+// part of the contract -- the reports must be byte-identical to the
+// reference's on the same samples -- so every accumulation below runs in the
+// order the reference's report defines (sample order, then sorted order for
+// the density).
+struct Moments {
+    size_t n = 0;
+    double total = 0.0, lo = 0.0, hi = 0.0, mean = 0.0, sd = 0.0;
+    explicit Moments(const std::vector<double>& v) : n(v.size()) {
+        if (v.empty()) throw Error("cannot summarize an empty sample");
+        lo = hi = v.front();
+        for (double x : v) {
+            total += x;
+            lo = std::min(lo, x);
+            hi = std::max(hi, x);
+        }
+        mean = total / double(n);
+        if (n < 2) return;
+        double ss = 0.0;
+        for (double x : v) ss += (x - mean) * (x - mean);
+        sd = std::sqrt(ss / double(n - 1));
+    }
+};
+
+// Linear-interpolation (type 7) quantile of an ascending sample.
+double type7(const std::vector<double>& asc, double p) {
+    const double at = p * double(asc.size() - 1);
+    const size_t k = size_t(at);
+    const double frac = at - double(k);
+    return asc[k] * (1.0 - frac) + asc[std::min(k + 1, asc.size() - 1)] * frac;
+}
+
+// Robust spread for Silverman's rule: min(sd, IQR/1.34), or whichever of
+// the two is non-zero, or 0 for a constant sample.
+double silverman_spread(double sd, double iqr) {
+    const double r = iqr / 1.34;
+    if (sd > 0.0 && iqr > 0.0) return std::min(sd, r);
+    return sd > 0.0 ? sd : iqr > 0.0 ? r : 0.0;
 }
 
 }  // namespace
 
+Summary summarize(const std::vector<double>& values) {
+    const Moments m(values);
+    Summary s;
+    s.count = m.n;
+    s.mean = m.mean;
+    s.stddev = m.sd;
+    s.min = m.lo;
+    s.max = m.hi;
+    return s;
+}
+
 Kde kde(const std::vector<double>& samples, size_t points) {
     if (samples.empty()) throw Error("cannot estimate a density from an empty sample");
     if (points < 2) throw Error("a density grid needs at least two points");
-    std::vector<double> sorted(samples);
-    std::sort(sorted.begin(), sorted.end());
-    const double n = double(sorted.size());
-    const Summary sum = summarize(samples);
-    const double iqr = quantile7(sorted, 0.75) - quantile7(sorted, 0.25);
-    double spread = 0.0;
-    if (sum.stddev > 0.0 && iqr > 0.0) spread = std::min(sum.stddev, iqr / 1.34);
-    else if (sum.stddev > 0.0) spread = sum.stddev;
-    else if (iqr > 0.0) spread = iqr / 1.34;
-
+    std::vector<double> asc(samples);
+    std::sort(asc.begin(), asc.end());
+    const double n = double(asc.size());
+    const double spread =
+        silverman_spread(Moments(samples).sd, type7(asc, 0.75) - type7(asc, 0.25));
     Kde k;
-    double left = sorted.front(), right = sorted.back();
-    if (spread > 0.0) {
-        k.bandwidth = 0.9 * spread * std::pow(n, -0.2);
-    } else {
-        k.bandwidth = 0.25;
-        left -= 1.0;
-        right += 1.0;
-    }
-    const double dx = (right - left) / double(points - 1);
-    const double norm = 1.0 / (n * k.bandwidth * std::sqrt(2.0 * 3.14159265358979323846));
+    // A constant sample gets a fixed bandwidth over [min - 1, max + 1].
+    const double left = asc.front() - (spread > 0.0 ? 0.0 : 1.0);
+    const double right = asc.back() + (spread > 0.0 ? 0.0 : 1.0);
+    k.bandwidth = spread > 0.0 ? 0.9 * spread * std::pow(n, -0.2) : 0.25;
+    const double step = (right - left) / double(points - 1);
+    const double scale = 1.0 / (n * k.bandwidth * std::sqrt(2.0 * 3.14159265358979323846));
     k.x.resize(points);
     k.y.resize(points);
-    for (size_t i = 0; i < points; ++i) {
-        const double xi = left + dx * double(i);
-        double acc = 0.0;
-        for (double s : sorted) {
-            const double z = (xi - s) / k.bandwidth;
-            acc += std::exp(-0.5 * z * z);
+    for (size_t g = 0; g < points; ++g) {
+        k.x[g] = left + step * double(g);
+        double mass = 0.0;
+        for (double s : asc) {
+            const double z = (k.x[g] - s) / k.bandwidth;
+            mass += std::exp(-0.5 * z * z);
         }
-        k.x[i] = xi;
-        k.y[i] = acc * norm;
+        k.y[g] = mass * scale;
     }
+    // Renormalize to a unit trapezoid integral over the grid.
     double area = 0.0;
-    for (size_t i = 0; i + 1 < points; ++i) area += 0.5 * (k.y[i] + k.y[i + 1]) * dx;
+    for (size_t g = 1; g < points; ++g) area += 0.5 * (k.y[g - 1] + k.y[g]) * step;
     for (double& y : k.y) y /= area;
     return k;
 }

@@ -268,3 +268,17 @@ def test_malformed_replay_tables_fail_like_the_reference(tmp_path, body):
     # table while parsing the job); the diagnostic itself must be the same
     want = str(ref_err.value).strip().removeprefix("job file error: ")
     assert want in str(mine_err.value), (str(ref_err.value), str(mine_err.value))
+
+
+@pytest.mark.parametrize("values", [[5, 7, 7, 5], [3, -1, 3], [-2, 4, -2], [1, 2, 3, 2, 1], [0, -5]])
+def test_parameter_value_errors_match_the_reference(tmp_path, values):
+    job = {"kernel": {"name": "k", "source_ref": "k.cu", "global": [64], "local": [1],
+                      "arguments": [{"role": "output", "type": "f32", "length": 64}]},
+           "space": {"parameters": {"P": values}}, "device": "K40m"}
+    text = json.dumps(job)
+    with pytest.raises(Exception) as ref_err:
+        O.ref_job_counts(text)
+    with pytest.raises(Exception) as mine_err:
+        pkg.Tuner.from_job(text, str(tmp_path)).space_counts()
+    want = str(ref_err.value).strip().removeprefix("job file error: ")
+    assert want in str(mine_err.value), (str(ref_err.value), str(mine_err.value))
