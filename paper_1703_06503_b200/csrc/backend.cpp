@@ -83,6 +83,9 @@ struct Plan {
     double rel_tol = -1.0;  // family tolerance override (< 0: backend options)
     unsigned box[2] = {0, 0};
     double compile_cost = 1.0;  // relative NVRTC cost estimate (CompileService ordering)
+    // SGEMM TAILK: 1-D grid of whole tiles + K-split tail tiles (ptxgen_gemm.cpp)
+    bool tailk = false;
+    unsigned tiles_x = 0, tiles_y = 0, ktiles = 0, tile_floats = 0;
 };
 
 // Relative NVRTC cost of a kernel whose fully unrolled body holds `n` FMAs
@@ -150,6 +153,10 @@ struct ktc_backend {
     std::unique_ptr<Inputs> in;
     std::map<std::string, KernelSource> custom_sources;  // path -> source
     std::vector<ModuleEntry> modules;
+    // SGEMM TAILK scratch: partial tiles of the split tail and their arrival
+    // counters (zeroed on allocation; every tile's last split resets its own).
+    CUdeviceptr tail_ws = 0, tail_cnt = 0;
+    size_t tail_ws_bytes = 0, tail_cnt_bytes = 0;
     // Host copy of the reference bound by ktc_backend_set_reference, so it
     // survives a context reset (a sticky fault frees every device buffer;
     // the inputs are rebuilt and the reference re-uploaded).
@@ -518,6 +525,8 @@ int ensure_inputs(ktc_backend* be, const ktc_request* r, Family fam) {
     if (be->ctx->sticky) {
         free_inputs(be);
         be->modules.clear();  // died with the context
+        be->tail_ws = be->tail_cnt = 0;
+        be->tail_ws_bytes = be->tail_cnt_bytes = 0;
         int st = ktc_reset(be->ctx);
         if (st) return st;
     }
@@ -692,6 +701,16 @@ int gemm_occ_policy() {
     return v;
 }
 
+// Split-K tail wave for the PTX-generated SGEMM (TAILK); KTC_GEMM_TAIL=0
+// disables it.  The NVRTC build (gemm.cu) has no tail split.
+int gemm_tail_policy() {
+    static const int v = [] {
+        const char* e = std::getenv("KTC_GEMM_TAIL");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 // Packed FFMA2 outer products (gemm.cu F2); KTC_GEMM_F2 overrides.
 int gemm_f2_policy() {
     static const int v = [] {
@@ -753,6 +772,20 @@ bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
     p->config.push_back(define("OCC", gemm_occ_policy()));
     p->config.push_back(define("F2", gemm_f2_policy()));
     p->smem = dbuf ? 2 * tile_bytes : tile_bytes;
+    // Compiled in only where a tail can matter: problems of at most ~8
+    // waves at two CTAs per SM (the decision to split is made at launch
+    // from the kernel's real occupancy).
+    const long long tiles = (I.M / MWG) * (I.N / NWG);
+    if (gemm_tail_policy() && gemm_source().ptx_generator &&
+        tiles <= 16LL * be->ctx->limits.sm_count) {
+        p->config.push_back(define("TAILK", 1));
+        p->tailk = true;
+        p->smem += 16;  // the arrival flag after the staged tiles
+        p->tiles_x = unsigned(I.M / MWG);
+        p->tiles_y = unsigned(I.N / NWG);
+        p->ktiles = unsigned(I.K / KWG);
+        p->tile_floats = unsigned(MWG * NWG);
+    }
     p->compile_cost = unrolled_cost(double((MWG / MDIMC) * (NWG / NDIMC) * KWI) + 64.0);
     if (p->smem > be->ctx->limits.smem_per_block_optin) {
         *why = "needs " + std::to_string(p->smem) + " bytes of shared memory";
@@ -938,6 +971,8 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
     int iX = 0, iY = 0, iP = 0, iM = 0, iN = 0, iK = 0;
     float fW = 0, fA = 0, fB = 0;
     CUdeviceptr pImg = 0, pOut = 0, pA = 0, pB = 0, pC = 0;
+    CUdeviceptr tk_ws = 0, tk_cnt = 0;
+    unsigned tk_full = 0, tk_splits = 1, tk_gx = 1, tk_kt = 1;
     std::vector<long long> scal_i;  // custom scalars
     std::vector<float> scal_f;
     std::vector<CUdeviceptr> ptrs;
@@ -1018,6 +1053,53 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
         pC = I.dev[7];
         pOut = I.out[0];
         params = {&iM, &iN, &iK, &fA, &fB, &pA, &pB, &pC, &pOut};
+        if (plan.tailk) {
+            // Whole waves of tiles stay whole; a tail wave that would leave
+            // most of the GPU idle is cut along K into `splits` CTAs per tile.
+            int occ = 0;
+            d.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn->fn,
+                                                          int(plan.block[0] * plan.block[1]),
+                                                          size_t(plan.smem));
+            const unsigned tiles = plan.tiles_x * plan.tiles_y;
+            const unsigned slots = unsigned(std::max(occ, 0)) * unsigned(ctx->limits.sm_count);
+            const unsigned rem = slots ? tiles % slots : 0;
+            unsigned splits = 1;
+            if (rem && 2 * rem <= slots)
+                splits = std::min({slots / rem, plan.ktiles, 8u});
+            if (splits < 2) splits = 1;
+            tk_full = splits > 1 ? tiles - rem : tiles;
+            tk_splits = splits;
+            tk_gx = plan.tiles_x;
+            tk_kt = plan.ktiles;
+            const size_t ws = size_t(tiles - tk_full) * splits * plan.tile_floats * 4;
+            const size_t cn = size_t(tiles - tk_full) * 4;
+            if (ws > be->tail_ws_bytes) {
+                if (be->tail_ws) d.cuMemFree(be->tail_ws);
+                be->tail_ws = 0;
+                be->tail_ws_bytes = 0;
+                if (d.cuMemAlloc(&be->tail_ws, ws) != CUDA_SUCCESS) {
+                    set_msg(out, "cannot allocate the split-K tail workspace");
+                    return KTC_OK;
+                }
+                be->tail_ws_bytes = ws;
+            }
+            if (cn > be->tail_cnt_bytes) {
+                if (be->tail_cnt) d.cuMemFree(be->tail_cnt);
+                be->tail_cnt = 0;
+                be->tail_cnt_bytes = 0;
+                if (d.cuMemAlloc(&be->tail_cnt, cn) != CUDA_SUCCESS ||
+                    d.cuMemsetD32Async(be->tail_cnt, 0, cn / 4, ctx->stream) != CUDA_SUCCESS) {
+                    set_msg(out, "cannot allocate the split-K tail counters");
+                    return KTC_OK;
+                }
+                be->tail_cnt_bytes = cn;
+            }
+            tk_ws = be->tail_ws ? be->tail_ws : pOut;  // never read without a tail
+            tk_cnt = be->tail_cnt ? be->tail_cnt : pOut;
+            params.insert(params.end(), {&tk_ws, &tk_cnt, &tk_full, &tk_splits, &tk_gx, &tk_kt});
+            plan.grid[0] = tk_full + (tiles - tk_full) * splits;
+            plan.grid[1] = 1;
+        }
         if (plan.tma_mode == 2) {
             params.push_back(&tmap);
             params.push_back(&tmap2);
@@ -1087,6 +1169,8 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
         // configuration starts clean (inputs are rebuilt lazily).
         if (ctx->sticky && !ktc::g_isolated_worker) {
             be->modules.clear();  // modules died with the context
+            be->tail_ws = be->tail_cnt = 0;
+            be->tail_ws_bytes = be->tail_cnt_bytes = 0;
             free_inputs(be);
             int rs = ktc_reset(ctx);
             if (rs) return rs;
@@ -1205,6 +1289,9 @@ void ktc_backend_close(ktc_backend* be) {
     free_inputs(be);
     trace_phase("close: free inputs", t0);
     if (!be->ctx->sticky) {
+        driver().cuCtxSetCurrent(be->ctx->cu);
+        if (be->tail_ws) driver().cuMemFree(be->tail_ws);
+        if (be->tail_cnt) driver().cuMemFree(be->tail_cnt);
         // Synchronous: a background unloader was measured to stall the next
         // job's 134 MB H2D copy by up to 0.8 s (driver serialization).
         driver().cuCtxSetCurrent(be->ctx->cu);

@@ -40,7 +40,7 @@ long long dv(const Defines& ds, const char* name, bool required, long long fallb
 
 struct GemmGen {
     int MWG, NWG, KWG, MDIMC, NDIMC, SA, SB, MDIMA, NDIMB, STRM, STRN, VWM, VWN, KWI;
-    int DBUF, OCC, F2;
+    int DBUF, OCC, F2, TAILK;
 };
 
 GemmGen parse(const Defines& c) {
@@ -62,6 +62,7 @@ GemmGen parse(const Defines& c) {
     g.DBUF = int(dv(c, "DBUF", false, 0));
     g.OCC = int(dv(c, "OCC", false, 0));
     g.F2 = int(dv(c, "F2", false, 1));
+    g.TAILK = int(dv(c, "TAILK", false, 0));
     return g;
 }
 
@@ -182,8 +183,56 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
     const std::string tx = x.r(), ty = x.r(), cx = x.r(), cy = x.r(), m0 = x.r(), n0 = x.r();
     x.op("mov.u32 " + tx + ", %tid.x");
     x.op("mov.u32 " + ty + ", %tid.y");
-    x.op("mov.u32 " + cx + ", %ctaid.x");
-    x.op("mov.u32 " + cy + ", %ctaid.y");
+    // K range of this CTA: the whole K, or (TAILK) one split of a tail tile.
+    const std::string kbeg = x.r(), kend = x.r();
+    // TAILK (host switch, part of the compile key): a 1-D grid of `full`
+    // whole tiles followed by the remaining (tail) tiles cut into `splits`
+    // K-ranges each, so the last wave fills the GPU; a tail CTA stores its
+    // partial tile, and the last of a tile's splits to arrive (counter)
+    // reduces the partials in split order and runs the epilogue.
+    std::string dW, dCnt, rFull, rSplits, pnorm, tail_t, split;
+    if (g.TAILK) {
+        dW = x.d();
+        dCnt = x.d();
+        rFull = x.r();
+        rSplits = x.r();
+        const std::string rGX = x.r(), rKT = x.r();
+        x.op("ld.param.u64 " + dW + ", [" + P + "9]");
+        x.op("ld.param.u64 " + dCnt + ", [" + P + "10]");
+        x.op("ld.param.u32 " + rFull + ", [" + P + "11]");
+        x.op("ld.param.u32 " + rSplits + ", [" + P + "12]");
+        x.op("ld.param.u32 " + rGX + ", [" + P + "13]");
+        x.op("ld.param.u32 " + rKT + ", [" + P + "14]");
+        x.op("cvta.to.global.u64 " + dW + ", " + dW);
+        x.op("cvta.to.global.u64 " + dCnt + ", " + dCnt);
+        const std::string b = x.r(), u = x.r(), tile = x.r(), kt0 = x.r(), kt1 = x.r();
+        tail_t = x.r();
+        split = x.r();
+        pnorm = x.p();
+        x.op("mov.u32 " + b + ", %ctaid.x");
+        x.op("setp.lt.u32 " + pnorm + ", " + b + ", " + rFull);
+        x.op("sub.u32 " + u + ", " + b + ", " + rFull);
+        x.op("div.u32 " + tail_t + ", " + u + ", " + rSplits);   // tail tile (valid when !pnorm)
+        x.op("rem.u32 " + split + ", " + u + ", " + rSplits);
+        x.op("add.u32 " + tile + ", " + tail_t + ", " + rFull);
+        x.op("selp.u32 " + tile + ", " + b + ", " + tile + ", " + pnorm);
+        x.op("rem.u32 " + cx + ", " + tile + ", " + rGX);
+        x.op("div.u32 " + cy + ", " + tile + ", " + rGX);
+        // split j covers K-tiles [j*kt/s, (j+1)*kt/s)
+        x.op("mul.lo.u32 " + kt0 + ", " + split + ", " + rKT);
+        x.op("div.u32 " + kt0 + ", " + kt0 + ", " + rSplits);
+        x.op("mad.lo.u32 " + kt1 + ", " + split + ", " + rKT + ", " + rKT);
+        x.op("div.u32 " + kt1 + ", " + kt1 + ", " + rSplits);
+        x.op("mul.lo.u32 " + kt0 + ", " + kt0 + ", " + imm(g.KWG));
+        x.op("mul.lo.u32 " + kt1 + ", " + kt1 + ", " + imm(g.KWG));
+        x.op("selp.u32 " + kbeg + ", 0, " + kt0 + ", " + pnorm);
+        x.op("selp.u32 " + kend + ", " + rK + ", " + kt1 + ", " + pnorm);
+    } else {
+        x.op("mov.u32 " + cx + ", %ctaid.x");
+        x.op("mov.u32 " + cy + ", %ctaid.y");
+        x.op("mov.u32 " + kbeg + ", 0");
+        x.op("mov.u32 " + kend + ", " + rK);
+    }
     x.op("mul.lo.u32 " + m0 + ", " + cx + ", " + imm(g.MWG));
     x.op("mul.lo.u32 " + n0 + ", " + cy + ", " + imm(g.NWG));
     const std::string tid = x.r();
@@ -343,10 +392,8 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
             x.op("add.u32 " + b_buf1 + ", " + b_buf0 + ", " + imm((long long)g.KWG * g.NWG * 4));
         }
     }
-    const std::string zero = x.r();
-    x.op("mov.u32 " + zero + ", 0");
-    if (g.DBUF) issue(zero, a_buf0, b_buf0);
-    else if (ca.on || cb.on) fetch(zero);
+    if (g.DBUF) issue(kbeg, a_buf0, b_buf0);
+    else if (ca.on || cb.on) fetch(kbeg);
 
     // Fragment offsets within a K-row (bytes): a: mv*VWM*4 = abase + aimm(mi),
     // b: nv*VWN*4 = bbase + bimm(ni) (the thread part in a register, the
@@ -359,18 +406,18 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
 
     // ---- k0 loop
     const std::string k0 = x.r(), buf = x.r(), lk0 = x.label(), lend = x.label();
-    x.op("mov.u32 " + k0 + ", 0");
+    x.op("mov.u32 " + k0 + ", " + kbeg);
     x.op("mov.u32 " + buf + ", 0");
     {
         const std::string pe = x.p();
-        x.op("setp.ge.u32 " + pe + ", " + k0 + ", " + rK);
+        x.op("setp.ge.u32 " + pe + ", " + k0 + ", " + kend);
         x.op("@" + pe + " bra " + lend);
     }
     x.lab(lk0);
     x.op(".pragma \"nounroll\"");
     const std::string knext = x.r(), pmore = x.p();
     x.op("add.u32 " + knext + ", " + k0 + ", " + imm(g.KWG));
-    x.op("setp.lt.u32 " + pmore + ", " + knext + ", " + rK);
+    x.op("setp.lt.u32 " + pmore + ", " + knext + ", " + kend);
     std::string acur, bcur;  // current tile base (shared u32)
     if (g.DBUF) {
         x.op("cp.async.wait_group 0");
@@ -525,6 +572,113 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
     x.op("@" + pmore + " bra " + lk0);
     x.lab(lend);
 
+    // ---- TAILK: partial tiles of the tail wave meet here
+    if (g.TAILK) {
+        const std::string lepi = x.label();
+        x.op("@" + pnorm + " bra " + lepi);
+        const long long tile_bytes = (long long)g.MWG * g.NWG * 4;
+        // this CTA's partial: W + ((tail_t * s + split) * tile_bytes)
+        const std::string slot = x.r(), wmine = x.d(), wtile = x.d(), tmp = x.d();
+        x.op("mad.lo.u32 " + slot + ", " + tail_t + ", " + rSplits + ", " + split);
+        x.op("mul.wide.u32 " + tmp + ", " + slot + ", " + imm(tile_bytes));
+        x.op("add.u64 " + wmine + ", " + dW + ", " + tmp);
+        const std::string tslot = x.r();
+        x.op("mul.lo.u32 " + tslot + ", " + tail_t + ", " + rSplits);
+        x.op("mul.wide.u32 " + tmp + ", " + tslot + ", " + imm(tile_bytes));
+        x.op("add.u64 " + wtile + ", " + dW + ", " + tmp);
+        // byte offset of (mi, e, ni) inside a tile: same element map as the epilogue
+        auto tile_off = [&](int mi, int e) {
+            const std::string mo = x.r();
+            x.op("shr.u32 " + mo + ", " + abase + ", 2");
+            x.op("add.u32 " + mo + ", " + mo + ", " + imm(aimm(mi) / 4 + e));
+            x.op("mul.lo.u32 " + mo + ", " + mo + ", " + imm((long long)g.NWG * 4));
+            x.op("add.u32 " + mo + ", " + mo + ", " + bbase);
+            const std::string d = x.d();
+            x.op("cvt.u64.u32 " + d + ", " + mo);
+            return d;
+        };
+        for (int mi = 0; mi < MVI; ++mi)
+            for (int e = 0; e < g.VWM; ++e) {
+                const std::string off = tile_off(mi, e), a = x.d();
+                x.op("add.u64 " + a + ", " + wmine + ", " + off);
+                for (int ni = 0; ni < NVI; ++ni) {
+                    std::vector<std::string> s(acc[size_t(mi * g.VWM + e)].begin() + ni * g.VWN,
+                                               acc[size_t(mi * g.VWM + e)].begin() + (ni + 1) * g.VWN);
+                    vst(x, "global", a, bimm(ni), s);
+                }
+            }
+        x.op("fence.acq_rel.gpu");
+        x.op("bar.sync 0");
+        const std::string ptid0 = x.p(), arrived = x.r(), cnt_a = x.d(), flag = x.r();
+        const long long flag_off = (long long)(g.SA * g.KWG * g.MWG + g.SB * g.KWG * g.NWG) * 4 *
+                                   (1 + g.DBUF);
+        {
+            const std::string d = x.d();
+            x.op("mov.u64 " + d + ", smem");
+            x.op("cvt.u32.u64 " + flag + ", " + d);
+            x.op("add.u32 " + flag + ", " + flag + ", " + imm(flag_off));
+        }
+        x.op("mul.wide.u32 " + cnt_a + ", " + tail_t + ", 4");
+        x.op("add.u64 " + cnt_a + ", " + dCnt + ", " + cnt_a);
+        x.op("setp.eq.u32 " + ptid0 + ", " + tid + ", 0");
+        {
+            const std::string skip = x.label();
+            x.op("@!" + ptid0 + " bra " + skip);
+            x.op("atom.acq_rel.gpu.global.add.u32 " + arrived + ", [" + cnt_a + "], 1");
+            x.op("st.shared.u32 [" + flag + "], " + arrived);
+            x.lab(skip);
+        }
+        x.op("bar.sync 0");
+        {
+            const std::string seen = x.r(), last = x.r(), plast = x.p();
+            x.op("ld.shared.u32 " + seen + ", [" + flag + "]");
+            x.op("sub.u32 " + last + ", " + rSplits + ", 1");
+            x.op("setp.ne.u32 " + plast + ", " + seen + ", " + last);
+            x.op("@" + plast + " ret");  // not the last split of this tile
+        }
+        x.op("fence.acq_rel.gpu");
+        {
+            const std::string skip = x.label();
+            x.op("@!" + ptid0 + " bra " + skip);
+            x.op("st.relaxed.gpu.global.u32 [" + cnt_a + "], 0");  // ready for the next launch
+            x.lab(skip);
+        }
+        // acc = 0 + partial[0] + partial[1] + ... in split order
+        // (deterministic; one rolled loop keeps the code small)
+        for (auto& row : acc)
+            for (auto& a : row) x.op("mov.f32 " + a + ", 0f00000000");
+        std::vector<std::string> offs;
+        for (int mi = 0; mi < MVI; ++mi)
+            for (int e = 0; e < g.VWM; ++e) offs.push_back(tile_off(mi, e));
+        const std::string j = x.r(), wj = x.d(), lj = x.label(), pj = x.p();
+        x.op("mov.u32 " + j + ", 0");
+        x.op("mov.u64 " + wj + ", " + wtile);
+        x.lab(lj);
+        x.op(".pragma \"nounroll\"");
+        {
+            size_t oi = 0;
+            for (int mi = 0; mi < MVI; ++mi)
+                for (int e = 0; e < g.VWM; ++e) {
+                    const std::string a = x.d();
+                    x.op("add.u64 " + a + ", " + wj + ", " + offs[oi++]);
+                    for (int ni = 0; ni < NVI; ++ni) {
+                        auto& row = acc[size_t(mi * g.VWM + e)];
+                        std::vector<std::string> v(static_cast<size_t>(g.VWN));
+                        for (auto& r : v) r = x.f();
+                        vld(x, "global.cg", a, bimm(ni), v);
+                        for (int q = 0; q < g.VWN; ++q)
+                            x.op("add.rn.f32 " + row[size_t(ni * g.VWN + q)] + ", " +
+                                 row[size_t(ni * g.VWN + q)] + ", " + v[size_t(q)]);
+                    }
+                }
+        }
+        x.op("add.u64 " + wj + ", " + wj + ", " + imm(tile_bytes));
+        x.op("add.u32 " + j + ", " + j + ", 1");
+        x.op("setp.lt.u32 " + pj + ", " + j + ", " + rSplits);
+        x.op("@" + pj + " bra " + lj);
+        x.lab(lepi);
+    }
+
     // ---- epilogue: Cout = alpha * acc (+ beta * Cin), VWN-wide along N
     const std::string pbeta = x.p();
     x.op("setp.neu.f32 " + pbeta + ", " + fBe + ", 0f00000000");
@@ -581,7 +735,12 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
       << "\t.param .u32 " << P << "0,\n\t.param .u32 " << P << "1,\n\t.param .u32 " << P
       << "2,\n\t.param .f32 " << P << "3,\n\t.param .f32 " << P << "4,\n\t.param .u64 .ptr .align 1 "
       << P << "5,\n\t.param .u64 .ptr .align 1 " << P << "6,\n\t.param .u64 .ptr .align 1 " << P
-      << "7,\n\t.param .u64 .ptr .align 1 " << P << "8\n)\n.maxntid " << NT << ", 1, 1\n"
+      << "7,\n\t.param .u64 .ptr .align 1 " << P << "8";
+    if (g.TAILK)
+        e << ",\n\t.param .u64 .ptr .align 1 " << P << "9,\n\t.param .u64 .ptr .align 1 " << P
+          << "10,\n\t.param .u32 " << P << "11,\n\t.param .u32 " << P << "12,\n\t.param .u32 " << P
+          << "13,\n\t.param .u32 " << P << "14";
+    e << "\n)\n.maxntid " << NT << ", 1, 1\n"
       << ".minnctapersm " << MINB << "\n{\n" << x.decls() << x.body() << "}\n";
     return e.str();
 }

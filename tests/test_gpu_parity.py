@@ -328,3 +328,21 @@ def test_sharded_executor_two_workers_on_one_device(built):
     for r in rows:
         run_best = r.time_ms if run_best is None else min(run_best, r.time_ms)
         assert r.best_so_far == run_best
+
+
+def test_gemm_split_k_tail_matches_oracle(backend):
+    """The split-K tail (TAILK): few tiles, long K -> the launch cuts every
+    tile's K range across CTAs, reduces the partials in split order and runs
+    the alpha/beta epilogue; outputs match the oracle (incl. beta != 0) and
+    the counters are reset so repeated launches stay correct."""
+    names = "MWG NWG KWG MDIMC NDIMC SA SB MDIMA NDIMB STRM STRN VWM VWN KWI".split()
+    rows = [(64, 64, 32, 16, 16, 1, 1, 16, 16, 0, 1, 4, 4, 8),
+            (128, 64, 16, 16, 8, 1, 1, 16, 8, 1, 1, 4, 2, 8),
+            (32, 32, 32, 8, 8, 0, 1, 8, 8, 0, 1, 2, 2, 2)]
+    for (m, n, k, a, b) in [(512, 512, 2048, 1.0, 0.0), (256, 384, 4096, 1.5, 0.5)]:
+        want = O.gemm_reference(m, n, k, a, b)
+        for row in rows:
+            cfg = dict(zip(names, row))
+            r = backend.evaluate(pkg.gemm_request(m, n, k, cfg, alpha=a, beta=b, reps=3))
+            assert r.ok and r.verification == "pass", (cfg, r)
+            assert O.verify(backend.read_output(m * n), want)["pass"], cfg
