@@ -203,6 +203,16 @@ int verify_pair(ktc_ctx* ctx, CUdeviceptr cand, CUdeviceptr ref, size_t count, i
 
 using namespace ktc;
 
+void ktc::retire_module(ktc_ctx* ctx, CUmodule mod) {
+    ctx->retired.push_back(mod);
+    if (ctx->retired.size() <= kRetiredCap) return;
+    const Driver& d = driver();
+    d.cuCtxSetCurrent(ctx->cu);
+    const size_t half = ctx->retired.size() / 2;
+    for (size_t i = 0; i < half; ++i) d.cuModuleUnload(ctx->retired[i]);
+    ctx->retired.erase(ctx->retired.begin(), ctx->retired.begin() + long(half));
+}
+
 extern "C" {
 
 int ktc_abi_version(void) { return KTC_ABI_VERSION; }
@@ -360,6 +370,11 @@ extern "C" {
 static void teardown_ctx(ktc_ctx* c, bool reset) {
     const Driver& d = driver();
     if (!c->cu) return;
+    if (!reset) {
+        d.cuCtxSetCurrent(c->cu);
+        for (CUmodule m : c->retired) d.cuModuleUnload(m);
+    }
+    c->retired.clear();
     const auto t0 = std::chrono::steady_clock::now();
     if (!reset)
         for (auto& b : c->free_blocks) d.cuMemFree(b.second);

@@ -50,6 +50,10 @@ struct ktc_ctx {
     std::vector<std::pair<size_t, CUdeviceptr>> free_blocks;
     size_t free_bytes = 0;
     unsigned epoch = 0;  // primary_ctx_epoch() when the resources were made
+    // Modules of closed backends, unloaded in bulk (ktc_retire_module):
+    // cuModuleUnload costs milliseconds per module, which a fresh job would
+    // otherwise pay at the end of every tuning job.
+    std::vector<CUmodule> retired;
 };
 
 struct ktc_fn {
@@ -59,6 +63,12 @@ struct ktc_fn {
 };
 
 namespace ktc {
+
+// Hands a loaded module to its (pooled) context for deferred unloading; the
+// oldest half is unloaded once more than kRetiredCap are waiting, the rest
+// when the context is torn down.
+void retire_module(ktc_ctx* ctx, CUmodule mod);
+constexpr size_t kRetiredCap = 4096;
 
 // Thread-local last-error plumbing shared by every layer.
 void set_error(const std::string& msg);
