@@ -1054,20 +1054,26 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
         pOut = I.out[0];
         params = {&iM, &iN, &iK, &fA, &fB, &pA, &pB, &pC, &pOut};
         if (plan.tailk) {
-            // Whole waves of tiles stay whole; a tail wave that would leave
-            // most of the GPU idle is cut along K into `splits` CTAs per tile.
+            // Split-K launch policy (tools/split_probe.py, DESIGN 4): with a
+            // long K and at most ~1.5 waves of whole tiles, every tile's K
+            // range is cut into `splits` CTAs (8192x256x8192: +12%); square
+            // problems up to 4096^3 and tail-only splits measured neutral or
+            // slower, so they run whole tiles.  KTC_GEMM_SPLIT=s forces s.
             int occ = 0;
             d.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn->fn,
                                                           int(plan.block[0] * plan.block[1]),
                                                           size_t(plan.smem));
             const unsigned tiles = plan.tiles_x * plan.tiles_y;
             const unsigned slots = unsigned(std::max(occ, 0)) * unsigned(ctx->limits.sm_count);
-            const unsigned rem = slots ? tiles % slots : 0;
             unsigned splits = 1;
-            if (rem && 2 * rem <= slots)
-                splits = std::min({slots / rem, plan.ktiles, 8u});
+            if (unsigned(I.K) >= 4096 && slots && 2 * tiles < 3 * slots) {
+                const unsigned want = std::max(2u, (5 * slots + tiles) / (2 * tiles));
+                splits = std::min({want, std::max(plan.ktiles / 8, 1u), 8u});
+            }
+            if (const char* e = std::getenv("KTC_GEMM_SPLIT"))
+                splits = std::min(unsigned(std::max(std::atoi(e), 1)), plan.ktiles);
             if (splits < 2) splits = 1;
-            tk_full = splits > 1 ? tiles - rem : tiles;
+            tk_full = splits > 1 ? 0 : tiles;
             tk_splits = splits;
             tk_gx = plan.tiles_x;
             tk_kt = plan.ktiles;

@@ -330,16 +330,23 @@ def test_sharded_executor_two_workers_on_one_device(built):
         assert r.best_so_far == run_best
 
 
-def test_gemm_split_k_tail_matches_oracle(backend):
-    """The split-K tail (TAILK): few tiles, long K -> the launch cuts every
+def test_gemm_split_k_tail_matches_oracle(backend, monkeypatch):
+    """The split-K launch (TAILK): few tiles, long K -> the launch cuts every
     tile's K range across CTAs, reduces the partials in split order and runs
     the alpha/beta epilogue; outputs match the oracle (incl. beta != 0) and
-    the counters are reset so repeated launches stay correct."""
+    the counters are reset so repeated launches stay correct.  Covers the
+    launch policy (K >= 4096) and forced split counts (KTC_GEMM_SPLIT, read
+    at every launch)."""
     names = "MWG NWG KWG MDIMC NDIMC SA SB MDIMA NDIMB STRM STRN VWM VWN KWI".split()
     rows = [(64, 64, 32, 16, 16, 1, 1, 16, 16, 0, 1, 4, 4, 8),
             (128, 64, 16, 16, 8, 1, 1, 16, 8, 1, 1, 4, 2, 8),
             (32, 32, 32, 8, 8, 0, 1, 8, 8, 0, 1, 2, 2, 2)]
-    for (m, n, k, a, b) in [(512, 512, 2048, 1.0, 0.0), (256, 384, 4096, 1.5, 0.5)]:
+    for (m, n, k, a, b, force) in [(512, 512, 2048, 1.0, 0.0, "3"), (256, 384, 4096, 1.5, 0.5, None),
+                                   (256, 384, 4096, 1.5, 0.5, "2"), (512, 256, 8192, 1.0, 0.0, None)]:
+        if force:
+            monkeypatch.setenv("KTC_GEMM_SPLIT", force)
+        else:
+            monkeypatch.delenv("KTC_GEMM_SPLIT", raising=False)
         want = O.gemm_reference(m, n, k, a, b)
         for row in rows:
             cfg = dict(zip(names, row))

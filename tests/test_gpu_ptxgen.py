@@ -48,7 +48,9 @@ print(json.dumps(out))
 
 
 def run(codegen: str) -> dict:
-    env = dict(os.environ, KTC_CONV_CODEGEN=codegen, KTC_GEMM_CODEGEN=codegen)
+    # The split-K tail (a launch-time policy of the generated SGEMM only)
+    # changes the accumulation order of split tiles; compare single chains.
+    env = dict(os.environ, KTC_CONV_CODEGEN=codegen, KTC_GEMM_CODEGEN=codegen, KTC_GEMM_TAIL="0")
     p = subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT)], env=env, capture_output=True,
                        text=True, timeout=1500)
     assert p.returncode == 0, p.stderr[-3000:]
