@@ -609,6 +609,26 @@ int conv_f2_policy() {
     return v;
 }
 
+// Conv register budget (ptxgen_conv MINCTA -> .minnctapersm): 0 = ptxas's
+// own choice, 1 = the shared-memory-limited CTA count, n > 1 = n CTAs per
+// SM.  KTC_CONV_MINCTA overrides.
+int conv_mincta_policy() {
+    static const int v = [] {
+        const char* e = std::getenv("KTC_CONV_MINCTA");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
+// Single-box TMA halo of exactly TY + 2H rows (else rounded up to 8 rows).
+bool conv_bh_exact() {
+    static const bool v = [] {
+        const char* e = std::getenv("KTC_CONV_BH_EXACT");
+        return e ? std::atoi(e) != 0 : false;
+    }();
+    return v;
+}
+
 bool plan_conv(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why) {
     const Dims I = dims_of(r, FAM_CONV);
     ParamView pv{r};
@@ -645,8 +665,11 @@ bool plan_conv(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
         const long long BW = (PWO + 2 * H + 3) / 4 * 4 + 4 * PAD;
         const long long TR = TY + 2 * H;
         const long long NB = (TR + 255) / 256;
-        const long long BH = ((TR + NB - 1) / NB + 7) / 8 * 8;
         const long long NP = TX / PWO;
+        // Boxes after the first start 128-B aligned (BH a multiple of 8);
+        // a single box may be exactly the halo height (conv_bh_exact()).
+        const long long BH = (NB == 1 && NP == 1 && conv_bh_exact()) ? TR
+                                                                     : ((TR + NB - 1) / NB + 7) / 8 * 8;
         const long long PF = BW * NB * BH;
         o.insert(o.end(), {define("PWO", PWO), define("BW", BW), define("BH", BH),
                            define("NB", NB), define("NP", NP), define("PF", PF)});
@@ -656,6 +679,15 @@ bool plan_conv(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
         p->box[1] = unsigned(BH);
     }
     p->smem = unsigned(smem_floats * 4);
+    // Register budget: ask ptxas for as many co-resident CTAs as shared
+    // memory and the thread limit allow (conv_mincta_policy()).
+    if (const int pol = conv_mincta_policy()) {
+        const long long per_sm = be->ctx->limits.smem_per_sm ? be->ctx->limits.smem_per_sm : 233472;
+        long long n = pol > 1 ? pol
+                              : std::min<long long>({32, 2048 / (XWG * YWG),
+                                                     per_sm / ((long long)p->smem + 1024)});
+        if (n > 1) o.push_back(define("MINCTA", n));
+    }
     p->compile_cost = unrolled_cost(double(XWPT * YWPT) * (UNR ? double(I.F) * I.F : 4.0));
     if (p->smem > be->ctx->limits.smem_per_block_optin) {
         *why = "needs " + std::to_string(p->smem) + " bytes of shared memory; the device allows " +
@@ -772,11 +804,10 @@ bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
     p->config.push_back(define("OCC", gemm_occ_policy()));
     p->config.push_back(define("F2", gemm_f2_policy()));
     p->smem = dbuf ? 2 * tile_bytes : tile_bytes;
-    // Compiled in only where a tail can matter: problems of at most ~8
-    // waves at two CTAs per SM (the decision to split is made at launch
-    // from the kernel's real occupancy).
+    // Compiled in only where the launch policy can split: K >= 2048 (every
+    // split keeps K/s >= 1024) and at most 16 tiles per SM.
     const long long tiles = (I.M / MWG) * (I.N / NWG);
-    if (gemm_tail_policy() && gemm_source().ptx_generator &&
+    if (gemm_tail_policy() && gemm_source().ptx_generator && I.K >= 2048 &&
         tiles <= 16LL * be->ctx->limits.sm_count) {
         p->config.push_back(define("TAILK", 1));
         p->tailk = true;
@@ -852,24 +883,26 @@ bool plan_custom(ktc_backend* be, const ktc_request* r, Plan* p, std::string* wh
 bool plan_gemm_tf32(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why) {
     const Dims I = dims_of(r, FAM_GEMM_TF32);
     ParamView pv{r};
-    long long BN, BK, STAGES;
+    long long BN, BK, STAGES, CG = 1;
     if (!pv.get("BN", &BN) || !pv.get("BK", &BK) || !pv.get("STAGES", &STAGES)) {
         *why = "the gemm_tf32 family needs BN, BK, STAGES";
         return false;
     }
+    pv.get("CG", &CG);  // optional: 1 (one CTA per tile) unless given
     if (!(BN == 64 || BN == 128 || BN == 256) || !(BK == 32 || BK == 64) || STAGES < 2 ||
-        STAGES > 8) {
+        STAGES > 8 || !(CG == 1 || CG == 2)) {
         *why = "gemm_tf32 configuration outside the family's parameter domain";
         return false;
     }
-    if (I.M % 128 || I.N % BN || I.K % BK) {
+    if (I.M % (128 * CG) || I.N % BN || I.K % BK) {
         *why = "problem size (" + std::to_string(I.M) + "x" + std::to_string(I.N) + "x" +
-               std::to_string(I.K) + ") is not a multiple of the (128, BN, BK) tile";
+               std::to_string(I.K) + ") is not a multiple of the (" + std::to_string(128 * CG) +
+               ", BN, BK) tile";
         return false;
     }
     p->ksrc = &tf32_source();
-    p->config = {define("BN", BN), define("BK", BK), define("STAGES", STAGES)};
-    p->smem = unsigned(STAGES * 4 * BK * (128 + BN) + 2048);
+    p->config = {define("BN", BN), define("BK", BK), define("STAGES", STAGES), define("CG", CG)};
+    p->smem = unsigned(STAGES * 4 * BK * (128 + BN / CG) + 2048);
     if (p->smem > be->ctx->limits.smem_per_block_optin) {
         *why = "needs " + std::to_string(p->smem) + " bytes of shared memory";
         return false;
@@ -1054,21 +1087,25 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
         pOut = I.out[0];
         params = {&iM, &iN, &iK, &fA, &fB, &pA, &pB, &pC, &pOut};
         if (plan.tailk) {
-            // Split-K launch policy (tools/split_probe.py, DESIGN 4): with a
-            // long K and at most ~1.5 waves of whole tiles, every tile's K
-            // range is cut into `splits` CTAs (8192x256x8192: +12%); square
-            // problems up to 4096^3 and tail-only splits measured neutral or
-            // slower, so they run whole tiles.  KTC_GEMM_SPLIT=s forces s.
-            int occ = 0;
-            d.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn->fn,
-                                                          int(plan.block[0] * plan.block[1]),
-                                                          size_t(plan.smem));
+            // Split-K launch policy (tools/split_probe.py, DESIGN 4): per-SM
+            // balance.  The tiles land ~evenly on the SMs, so a launch of c
+            // CTAs per SM runs ceil(c) rounds on the busiest SM; cutting every
+            // tile's K range into s CTAs (each K/s >= 1024) is worth it when
+            // it evens the rounds out by more than the partial-tile reduction
+            // costs (~3%).  8192x256x8192: 3.46 -> 6.92/7 tiles per SM, +12%;
+            // 2048^3 / 4096^3 winners already balanced -> whole tiles.
             const unsigned tiles = plan.tiles_x * plan.tiles_y;
-            const unsigned slots = unsigned(std::max(occ, 0)) * unsigned(ctx->limits.sm_count);
+            const unsigned sms = unsigned(std::max(ctx->limits.sm_count, 1));
+            const unsigned smax = std::min({8u, plan.ktiles, std::max(unsigned(I.K) / 1024u, 1u)});
             unsigned splits = 1;
-            if (unsigned(I.K) >= 4096 && slots && 2 * tiles < 3 * slots) {
-                const unsigned want = std::max(2u, (5 * slots + tiles) / (2 * tiles));
-                splits = std::min({want, std::max(plan.ktiles / 8, 1u), 8u});
+            double best = -1.0;
+            for (unsigned s = 1; s <= smax; ++s) {
+                const double c = double(tiles) * s / sms;
+                const double eff = c / std::ceil(c) * (s > 1 ? 0.97 : 1.0);
+                if (eff > best + 1e-9) {
+                    best = eff;
+                    splits = s;
+                }
             }
             if (const char* e = std::getenv("KTC_GEMM_SPLIT"))
                 splits = std::min(unsigned(std::max(std::atoi(e), 1)), plan.ktiles);

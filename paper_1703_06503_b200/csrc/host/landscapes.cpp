@@ -133,6 +133,7 @@ SearchSpace gemm_tf32_space() {
     s.add_parameter("BN", {64, 128, 256});
     s.add_parameter("BK", {32, 64});
     s.add_parameter("STAGES", {2, 3, 4, 6});
+    s.add_parameter("CG", {1, 2});  // 2: CTA pair (cta_group::2), 256 x BN tiles
     return s;
 }
 
@@ -141,11 +142,13 @@ KernelSpec gemm_tf32_kernel(const GemmProblem& p) {
     KernelSpec k;
     k.name = "gemm_tf32";
     k.source_ref = "gemm_tf32.cu";
-    // One 128-thread CTA per 128 x BN output tile: grid (M/128, N/BN).
+    // One 128-thread CTA per 128 x BN output tile: grid (M/128, N/BN); with
+    // CG = 2 the CTAs pair up along M (clusters of 2) and each stages half
+    // of B, hence the shared-memory expression.
     k.base_global = {p.m, p.n};
     k.base_local = {128, 1};
     k.modifiers = {{SizeTarget::global, SizeOp::divide, {"1", "BN"}}};
-    k.local_mem_expr = "STAGES * 4 * BK * (128 + BN) + 2048";
+    k.local_mem_expr = "STAGES * 4 * BK * (128 + BN / CG) + 2048";
     k.arguments = gemm_arguments(p);
     return k;
 }

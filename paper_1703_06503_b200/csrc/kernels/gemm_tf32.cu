@@ -19,10 +19,12 @@
 //   epi   all 4 warps: tcgen05.ld 32x32b (warp w owns TMEM lanes 32w..32w+31
 //         = rows), alpha/beta, 128-byte row segments stored to global.
 //
-// Parameters: BN (64, 128, 256), BK (32, 64), STAGES (2, 3, 4, 6).  The
-// tensor core reads the fp32 operand bits as TF32 (truncating the low 13
-// mantissa bits), hence the variant's own tolerance.
-// Block: 128 threads; grid (M/128, N/BN).
+// Parameters: BN (64, 128, 256), BK (32, 64), STAGES (2, 3, 4, 6), CG (1, 2:
+// CTA pair, tcgen05.mma.cta_group::2 with M = 256 -- half the operand bytes
+// per SM of a 128 x BN tile, the L2 -> SM traffic that bounds the 1-CTA
+// kernel at 2048^3).  The tensor core reads the fp32 operand bits as TF32
+// (truncating the low 13 mantissa bits), hence the variant's own tolerance.
+// Block: 128 threads; grid (M/128, N/BN), clusters of CG CTAs along x.
 
 
 typedef unsigned int u32;
@@ -68,6 +70,58 @@ __device__ __forceinline__ void tma_load_2d(u32 dst, const TensorMap* map, u32 b
         : "memory");
 }
 
+// CTA-pair (cta_group::2) forms: the TMA of either CTA completes its bytes on
+// the leader's barrier (a shared::cluster address from mapa), and the
+// leader's MMA commit arrives on the same-offset barrier of both CTAs.
+__device__ __forceinline__ void tma_load_2d_pair(u32 dst, const TensorMap* map, u32 bar_cluster,
+                                                 int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<u64>(map)), "r"(bar_cluster), "r"(x), "r"(y)
+        : "memory");
+}
+
+__device__ __forceinline__ u32 mapa_rank(u32 addr, u32 rank) {
+    u32 out;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(rank));
+    return out;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ u32 cluster_rank() {
+    u32 r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void umma_tf32_pair(u32 tmem_d, u64 adesc, u64 bdesc, u32 idesc,
+                                               u32 accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void umma_commit_pair(u32 bar) {
+    const unsigned short mask = 3;
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(bar),
+        "h"(mask)
+        : "memory");
+}
+
 // UMMA shared-memory descriptor for MN-major 32-bit operands (sm_100): the
 // only layout UMMA accepts for MN-major TF32 is SWIZZLE_128B_BASE32B
 // (128-byte MN rows, 32-byte swizzle atoms over 4-row K groups), which is
@@ -85,10 +139,11 @@ __device__ __forceinline__ u64 umma_desc(u32 addr, u32 lbo, u32 sbo) {
     return d;
 }
 
-// Instruction descriptor: D f32, A/B tf32, both MN-major, M=128, N=bn.
-__device__ __forceinline__ u32 make_idesc(u32 bn) {
+// Instruction descriptor: D f32, A/B tf32, both MN-major, M = m (128, or
+// 256 for a CTA pair), N = bn.
+__device__ __forceinline__ u32 make_idesc(u32 m, u32 bn) {
     return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) | ((bn >> 3) << 17) |
-           ((128u >> 4) << 24);
+           ((m >> 4) << 24);
 }
 
 __device__ __forceinline__ void umma_tf32(u32 tmem_d, u64 adesc, u64 bdesc, u32 idesc,
@@ -108,27 +163,37 @@ __device__ __forceinline__ void umma_commit(u32 bar) {
 }
 
 //@@KTC_BODY@@ -- instantiated once per configuration; KTC_ENTRY names the kernel.
+// CG = 1: one CTA per 128 x BN tile.  CG = 2: a CTA pair (cluster of 2 along
+// x, same TPC) per 256 x BN tile: CTA r loads A rows m0 + 128r.. and B
+// columns n0 + r*BN/2.., the leader (r = 0) issues M=256 MMAs that read both
+// CTAs' shared memory, and each CTA's TMEM receives its own 128 rows x BN.
 #define BM 128
 #define NT 128
+#define BNL (BN / CG)
 #define A_BOX_BYTES (BK * 128)
 #define A_STAGE_BYTES (4 * A_BOX_BYTES)
-#define B_STAGE_BYTES ((BN / 32) * A_BOX_BYTES)
+#define B_STAGE_BYTES ((BNL / 32) * A_BOX_BYTES)
 #define STAGE_BYTES (A_STAGE_BYTES + B_STAGE_BYTES)
 #define TMEM_COLS (BN < 32 ? 32 : BN)
 
 extern "C" __global__ void __launch_bounds__(NT, 1)
+#if CG == 2
+__cluster_dims__(2, 1, 1)
+#endif
 KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float beta,
           const float* __restrict__ A, const float* __restrict__ B,
           const float* __restrict__ Cin, float* __restrict__ Cout,
           const __grid_constant__ TensorMap tmap_a, const __grid_constant__ TensorMap tmap_b) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-byte alignment for SWIZZLE_128B atoms.
+    // 1024-byte alignment for SWIZZLE_128B atoms (same offset in both CTAs
+    // of a pair: the leader's MMA descriptors address the peer's operands).
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<u64>(smem_raw) + 1023) & ~u64(1023));
     u64* bars = reinterpret_cast<u64*>(smem + STAGES * STAGE_BYTES);  // full[S], empty[S], acc
     u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * STAGES + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const u32 rank = CG == 2 ? cluster_rank() : 0u;
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
     const int kblocks = K / BK;
     const u32 full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES),
@@ -144,15 +209,27 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<u64>(&tmap_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<u64>(&tmap_b)) : "memory");
     }
-    if (warp == 1) {  // TMEM allocation: one warp, power-of-two >= 32 columns
+    if (warp == 1) {  // TMEM allocation: one warp (the same warp in both CTAs of a pair)
+#if CG == 2
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"((u32)TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+#else
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
                      "r"((u32)TMEM_COLS)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+#endif
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+#if CG == 2
+    cluster_sync_all();  // both CTAs' barriers exist before any cross-CTA arrive
+#else
     __syncthreads();
+#endif
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const u32 tmem = *tmem_slot;
 
@@ -161,27 +238,38 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
     // K-block) instead of spinning on the accumulator barrier, which would
     // split the warp and steal issue slots from the elected lane.
     if (warp == 0) {
-        // ---- TMA producer ----
+        // ---- TMA producer (both CTAs of a pair; bytes land on the leader's full barrier) ----
         for (int kb = 0; kb < kblocks; ++kb) {
             if (lane == 0) {
                 const int s = kb % STAGES;
                 const u32 phase = (u32)((kb / STAGES) & 1);
                 mbar_wait(empty0 + 8 * s, phase ^ 1u);
                 const u32 full = full0 + 8 * s;
-                mbar_expect_tx(full, STAGE_BYTES);
+                if (rank == 0) mbar_expect_tx(full, CG * STAGE_BYTES);
                 const u32 sa = smem_u32(smem + s * STAGE_BYTES);
                 const u32 sb = sa + A_STAGE_BYTES;
+#if CG == 2
+                const u32 fullc = mapa_rank(full, 0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    tma_load_2d_pair(sa + j * A_BOX_BYTES, &tmap_a, fullc, m0 + 32 * j, kb * BK);
+#pragma unroll
+                for (int j = 0; j < BNL / 32; ++j)
+                    tma_load_2d_pair(sb + j * A_BOX_BYTES, &tmap_b, fullc,
+                                     n0 + (int)rank * BNL + 32 * j, kb * BK);
+#else
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
                     tma_load_2d(sa + j * A_BOX_BYTES, &tmap_a, full, m0 + 32 * j, kb * BK);
 #pragma unroll
                 for (int j = 0; j < BN / 32; ++j)
                     tma_load_2d(sb + j * A_BOX_BYTES, &tmap_b, full, n0 + 32 * j, kb * BK);
+#endif
             }
             __syncwarp();
         }
-    } else if (warp == 1) {
-        // ---- MMA issuer (one elected thread) ----
+    } else if (warp == 1 && rank == 0) {
+        // ---- MMA issuer (one elected thread of the leader CTA) ----
         for (int kb = 0; kb < kblocks; ++kb) {
             if (lane == 0) {
                 const int s = kb % STAGES;
@@ -194,17 +282,29 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
                     // K = 8 per MMA = two 4-row groups of 512 B.
                     const u64 ad = umma_desc(sa + kk * 1024, A_BOX_BYTES, 512);
                     const u64 bd = umma_desc(sb + kk * 1024, A_BOX_BYTES, 512);
-                    umma_tf32(tmem, ad, bd, make_idesc(BN), (kb | kk) != 0 ? 1u : 0u);
+#if CG == 2
+                    umma_tf32_pair(tmem, ad, bd, make_idesc(256, BN), (kb | kk) != 0 ? 1u : 0u);
+#else
+                    umma_tf32(tmem, ad, bd, make_idesc(128, BN), (kb | kk) != 0 ? 1u : 0u);
+#endif
                 }
+#if CG == 2
+                umma_commit_pair(empty0 + 8 * s);  // both CTAs' stage s reusable
+#else
                 umma_commit(empty0 + 8 * s);  // stage reusable once these MMAs retire
+#endif
             }
             __syncwarp();
         }
+#if CG == 2
+        if (lane == 0) umma_commit_pair(accb);  // both accumulator halves complete
+#else
         if (lane == 0) umma_commit(accb);  // accumulator complete
+#endif
         __syncwarp();
     }
 
-    // ---- epilogue: all warps ----
+    // ---- epilogue: all warps (each CTA of a pair owns 128 rows x BN in its TMEM) ----
     mbar_wait(accb, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int row = warp * 32 + lane;  // TMEM lane == tile row
@@ -244,15 +344,26 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+#if CG == 2
+    cluster_sync_relaxed();  // neither CTA frees TMEM / exits while its pair is still reading
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1) {
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"((u32)TMEM_COLS)
+                     : "memory");
+    }
+#else
     __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                      "r"((u32)TMEM_COLS)
                      : "memory");
     }
+#endif
 }
 #undef BM
 #undef NT
+#undef BNL
 #undef A_BOX_BYTES
 #undef A_STAGE_BYTES
 #undef B_STAGE_BYTES

@@ -35,7 +35,7 @@ namespace {
 
 struct ConvGen {
     int FS = 0, XWG = 0, YWG = 0, XWPT = 0, YWPT = 0, LOCAL = 0, VW = 1, PAD = 0, UNR = 1;
-    int GUARD = 0, OUT_VEC = 1, CF2 = 1;
+    int GUARD = 0, OUT_VEC = 1, CF2 = 1, MINCTA = 1;
     int SP = 0, PWO = 0, BW = 0, BH = 0, NB = 0, NP = 0, PF = 0;
 };
 
@@ -61,6 +61,7 @@ ConvGen parse(const Defines& problem, const Defines& c) {
     g.GUARD = int(def_value(c, "GUARD", false, 0));
     g.OUT_VEC = int(def_value(c, "OUT_VEC", false, 1));
     g.CF2 = int(def_value(c, "CF2", false, 1));
+    g.MINCTA = int(def_value(c, "MINCTA", false, 1));
     if (g.LOCAL == 1) g.SP = int(def_value(c, "SP", true));
     if (g.LOCAL == 2) {
         g.PWO = int(def_value(c, "PWO", true));
@@ -536,7 +537,7 @@ std::string emit_entry(const ConvGen& g, const std::string& name) {
       << "\t.param .u32 " << P << "0,\n\t.param .u32 " << P << "1,\n\t.param .f32 " << P
       << "2,\n\t.param .u64 .ptr .align 1 " << P << "3,\n\t.param .u32 " << P
       << "4,\n\t.param .u64 .ptr .align 1 " << P << "5,\n\t.param .align 64 .b8 " << P
-      << "6[128]\n)\n.maxntid " << NT << ", 1, 1\n.minnctapersm 1\n{\n"
+      << "6[128]\n)\n.maxntid " << NT << ", 1, 1\n.minnctapersm " << g.MINCTA << "\n{\n"
       << x.decls() << x.body() << "}\n";
     return e.str();
 }

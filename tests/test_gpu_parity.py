@@ -265,19 +265,21 @@ def test_gemm_tf32_tcgen05_configs(backend, m, n, k):
     (the variant's stated tolerance) against the fp32 oracle."""
     want = O.gemm_reference(m, n, k)
     seen = 0
-    for bn in (64, 128, 256):
-        for bk in (32, 64):
-            for st in (2, 3, 4, 6):
-                if n % bn or k % bk or st * 4 * bk * (128 + bn) + 2048 > 232448:
-                    continue
-                cfg = dict(BN=bn, BK=bk, STAGES=st)
-                r = backend.evaluate(pkg.gemm_request(m, n, k, cfg, tf32=True))
-                assert r.ok and r.verification == "pass", (cfg, r)
-                assert r.report["max_rel_error"] < 1e-3
-                rep = O.verify(backend.read_output(m * n), want, 1e-3, 1e-6)
-                assert rep["pass"], (cfg, rep)
-                seen += 1
-    assert seen >= 6
+    for cg in (1, 2):  # 2: CTA pair, tcgen05.mma.cta_group::2 (M = 256)
+        for bn in (64, 128, 256):
+            for bk in (32, 64):
+                for st in (2, 3, 4, 6):
+                    if m % (128 * cg) or n % bn or k % bk or \
+                            st * 4 * bk * (128 + bn // cg) + 2048 > 232448:
+                        continue
+                    cfg = dict(BN=bn, BK=bk, STAGES=st, CG=cg)
+                    r = backend.evaluate(pkg.gemm_request(m, n, k, cfg, tf32=True))
+                    assert r.ok and r.verification == "pass", (cfg, r)
+                    assert r.report["max_rel_error"] < 1e-3
+                    rep = O.verify(backend.read_output(m * n), want, 1e-3, 1e-6)
+                    assert rep["pass"], (cfg, rep)
+                    seen += 1
+    assert seen >= 12
 
 
 def test_prune_factor_early_out_keeps_winner_and_verification(built):

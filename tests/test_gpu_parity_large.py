@@ -97,7 +97,7 @@ def test_gemm_tf32_8192_matches_fp32_oracle(backend, golden):
     want = oracle_gemm(m, m, m)
     assert O.digest(want) == golden["gemm_digests_large"]["8192"]["digest"]
     for cfg in (dict(BN=256, BK=32, STAGES=2), dict(BN=128, BK=32, STAGES=4),
-                dict(BN=256, BK=64, STAGES=2)):
+                dict(BN=256, BK=64, STAGES=2), dict(BN=256, BK=32, STAGES=4, CG=2)):
         r = backend.evaluate(pkg.gemm_request(m, m, m, cfg, tf32=True))
         assert r.ok and r.verification == "pass", (cfg, r)
         assert r.report["max_rel_error"] < 1e-3

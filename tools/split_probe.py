@@ -38,6 +38,8 @@ def main():
     ap.add_argument("--top", type=int, default=200)
     ap.add_argument("--shapes", default="2048x2048x2048")
     ap.add_argument("--splits", default="0,1,2,3,4,6,8")
+    ap.add_argument("--per-tile", type=int, default=0,
+                    help="instead of --top: the N fastest configurations of each (MWG, NWG) tile shape")
     ap.add_argument("--child", nargs=2)
     a = ap.parse_args()
     if a.child:
@@ -48,6 +50,18 @@ def main():
     t = np.load(ROOT / "profiles/fullsearch_r01/gemm2048_times.npz")["times"]
     order = np.argsort(np.nan_to_num(t, nan=1e9))
     idx = [int(i) for i in order[:a.top]]
+    if a.per_tile:
+        sys.path.insert(0, str(ROOT))
+        import paper_1703_06503_b200 as pkg
+
+        space = pkg.Tuner.gemm(2048, 2048, 2048)
+        count, idx = {}, []
+        for i in order[:100000]:
+            c = pkg.parse_canonical(space.space_config(int(i)))
+            key = (c["MWG"], c["NWG"])
+            if count.get(key, 0) < a.per_tile:
+                count[key] = count.get(key, 0) + 1
+                idx.append(int(i))
     (ROOT / "gpurun_out").mkdir(exist_ok=True)
     for shape in a.shapes.split(","):
         m, n, k = (int(v) for v in shape.split("x"))
