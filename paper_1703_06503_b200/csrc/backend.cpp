@@ -18,6 +18,7 @@
 #include <cstring>
 #include <fstream>
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <thread>
 #include <map>
@@ -609,6 +610,15 @@ int conv_f2_policy() {
     return v;
 }
 
+// Diagnostic CTA timeline of the conv family (ptxgen_conv TRACE): when
+// KTC_CONV_TRACE names a directory, each evaluation's last timed launch
+// leaves per-CTA {start ns, end ns, smid, 0} in <dir>/conv_trace_<n>.bin
+// (header: grid x, grid y as u32).  Never set in tuning runs.
+const char* conv_trace_dir() {
+    static const char* v = std::getenv("KTC_CONV_TRACE");
+    return v && *v ? v : nullptr;
+}
+
 // Conv register budget (ptxgen_conv MINCTA -> .minnctapersm): 0 = ptxas's
 // own choice, 1 = the shared-memory-limited CTA count, n > 1 = n CTAs per
 // SM.  KTC_CONV_MINCTA overrides.
@@ -688,6 +698,7 @@ bool plan_conv(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
                                                      per_sm / ((long long)p->smem + 1024)});
         if (n > 1) o.push_back(define("MINCTA", n));
     }
+    if (conv_trace_dir()) o.push_back(define("TRACE", 1));
     p->compile_cost = unrolled_cost(double(XWPT * YWPT) * (UNR ? double(I.F) * I.F : 4.0));
     if (p->smem > be->ctx->limits.smem_per_block_optin) {
         *why = "needs " + std::to_string(p->smem) + " bytes of shared memory; the device allows " +
@@ -1004,7 +1015,7 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
     int iX = 0, iY = 0, iP = 0, iM = 0, iN = 0, iK = 0;
     float fW = 0, fA = 0, fB = 0;
     CUdeviceptr pImg = 0, pOut = 0, pA = 0, pB = 0, pC = 0;
-    CUdeviceptr tk_ws = 0, tk_cnt = 0;
+    CUdeviceptr tk_ws = 0, tk_cnt = 0, trace_buf = 0;
     unsigned tk_full = 0, tk_splits = 1, tk_gx = 1, tk_kt = 1;
     std::vector<long long> scal_i;  // custom scalars
     std::vector<float> scal_f;
@@ -1054,6 +1065,14 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
         iP = I.ipitch;
         pOut = I.out[0];
         params = {&iX, &iY, &fW, &pImg, &iP, &pOut, &tmap};
+        if (conv_trace_dir()) {
+            const size_t tb = size_t(plan.grid[0]) * plan.grid[1] * 32;
+            if (d.cuMemAlloc(&trace_buf, tb) != CUDA_SUCCESS) {
+                set_msg(out, "cannot allocate the conv trace buffer");
+                return KTC_OK;
+            }
+            params.push_back(&trace_buf);
+        }
     } else if (fam == FAM_GEMM || fam == FAM_GEMM_TF32) {
         if (plan.tma_mode == 2) {
             auto encode = [&](CUtensorMap* m, CUdeviceptr base, int inner, int outer) {
@@ -1201,6 +1220,23 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
     st = ktc_launch_timed_pruned(ctx, fn, plan.grid, plan.block, plan.smem, params.data(),
                                  be->opts.warmup, reps, be->opts.flush_l2, bar, &best, all.data(),
                                  &reps_done);
+    if (trace_buf) {
+        static std::atomic<int> trace_n{0};
+        const size_t n = size_t(plan.grid[0]) * plan.grid[1];
+        std::vector<unsigned long long> host(n * 4);
+        if (!st && d.cuCtxSynchronize() == CUDA_SUCCESS &&
+            d.cuMemcpyDtoH(host.data(), trace_buf, n * 32) == CUDA_SUCCESS) {
+            const std::string path = std::string(conv_trace_dir()) + "/conv_trace_" +
+                                     std::to_string(trace_n++) + ".bin";
+            if (FILE* f = std::fopen(path.c_str(), "wb")) {
+                const unsigned hdr[2] = {plan.grid[0], plan.grid[1]};
+                std::fwrite(hdr, sizeof(hdr), 1, f);
+                std::fwrite(host.data(), 32, n, f);
+                std::fclose(f);
+            }
+        }
+        d.cuMemFree(trace_buf);
+    }
     double sum = 0.0;
     for (int k = 0; k < reps_done; ++k) sum += all[size_t(k)];
     out->mean_ms = sum / double(std::max(1, reps_done));

@@ -35,7 +35,7 @@ namespace {
 
 struct ConvGen {
     int FS = 0, XWG = 0, YWG = 0, XWPT = 0, YWPT = 0, LOCAL = 0, VW = 1, PAD = 0, UNR = 1;
-    int GUARD = 0, OUT_VEC = 1, CF2 = 1, MINCTA = 1;
+    int GUARD = 0, OUT_VEC = 1, CF2 = 1, MINCTA = 1, TRACE = 0;
     int SP = 0, PWO = 0, BW = 0, BH = 0, NB = 0, NP = 0, PF = 0;
 };
 
@@ -62,6 +62,7 @@ ConvGen parse(const Defines& problem, const Defines& c) {
     g.OUT_VEC = int(def_value(c, "OUT_VEC", false, 1));
     g.CF2 = int(def_value(c, "CF2", false, 1));
     g.MINCTA = int(def_value(c, "MINCTA", false, 1));
+    g.TRACE = int(def_value(c, "TRACE", false, 0));
     if (g.LOCAL == 1) g.SP = int(def_value(c, "SP", true));
     if (g.LOCAL == 2) {
         g.PWO = int(def_value(c, "PWO", true));
@@ -151,6 +152,25 @@ std::string emit_entry(const ConvGen& g, const std::string& name) {
     x.op("mov.u32 " + ty + ", %tid.y");
     x.op("mov.u32 " + cx + ", %ctaid.x");
     x.op("mov.u32 " + cy + ", %ctaid.y");
+    // TRACE (diagnostic build, KTC_CONV_TRACE): thread (0,0) records the
+    // CTA's start and end %globaltimer and its SM in trace[4 * linear_cta].
+    std::string trace_slot, trace_t0, trace_lead;
+    if (g.TRACE) {
+        trace_slot = x.d();
+        trace_t0 = x.d();
+        trace_lead = x.p();
+        const std::string lin = x.r(), nx = x.r(), o = x.r(), tb = x.d(), t = x.r();
+        x.op("mov.u32 " + nx + ", %nctaid.x");
+        x.op("mad.lo.u32 " + lin + ", " + cy + ", " + nx + ", " + cx);
+        x.op("ld.param.u64 " + tb + ", [" + P + "7]");
+        x.op("cvta.to.global.u64 " + tb + ", " + tb);
+        x.op("mul.wide.u32 " + trace_slot + ", " + lin + ", 32");
+        x.op("add.u64 " + trace_slot + ", " + trace_slot + ", " + tb);
+        x.op("or.b32 " + t + ", " + tx + ", " + ty);
+        x.op("setp.eq.u32 " + trace_lead + ", " + t + ", 0");
+        x.op("mov.u64 " + trace_t0 + ", %globaltimer");
+        (void)o;
+    }
     x.op("mul.lo.u32 " + x0 + ", " + cx + ", " + imm(TX));
     x.op("mul.lo.u32 " + y0 + ", " + cy + ", " + imm(TY));
     // Column of group gi (floats, relative to the tile): (gi*XWG + tx) * VW.
@@ -530,6 +550,15 @@ std::string emit_entry(const ConvGen& g, const std::string& name) {
         }
         x.lab(next);
     }
+    if (g.TRACE) {
+        const std::string t1 = x.d(), sm = x.r(), sm64 = x.d();
+        x.op("bar.sync 0");
+        x.op("mov.u64 " + t1 + ", %globaltimer");
+        x.op("mov.u32 " + sm + ", %smid");
+        x.op("cvt.u64.u32 " + sm64 + ", " + sm);
+        x.op("@" + trace_lead + " st.global.v2.u64 [" + trace_slot + "], {" + trace_t0 + ", " + t1 + "}");
+        x.op("@" + trace_lead + " st.global.u64 [" + trace_slot + "+16], " + sm64);
+    }
     x.op("ret");
 
     std::ostringstream e;
@@ -537,7 +566,8 @@ std::string emit_entry(const ConvGen& g, const std::string& name) {
       << "\t.param .u32 " << P << "0,\n\t.param .u32 " << P << "1,\n\t.param .f32 " << P
       << "2,\n\t.param .u64 .ptr .align 1 " << P << "3,\n\t.param .u32 " << P
       << "4,\n\t.param .u64 .ptr .align 1 " << P << "5,\n\t.param .align 64 .b8 " << P
-      << "6[128]\n)\n.maxntid " << NT << ", 1, 1\n.minnctapersm " << g.MINCTA << "\n{\n"
+      << "6[128]" << (g.TRACE ? std::string(",\n\t.param .u64 ") + P + "7" : std::string())
+      << "\n)\n.maxntid " << NT << ", 1, 1\n.minnctapersm " << g.MINCTA << "\n{\n"
       << x.decls() << x.body() << "}\n";
     return e.str();
 }
