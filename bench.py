@@ -589,19 +589,24 @@ def tuned_block(pkg, local, threads, sample_best, peaks) -> dict:
             "frac": gbs / peaks["hbm_gbs"] if bound == "hbm" else gflops / fp32_peak,
             "dram_bytes": (entry or {}).get("dram_bytes"),
         }
-    for size, g in sorted(table.get("gemm", {}).items(), key=lambda kv: int(kv[0])):
-        m = int(size)
-        req = pkg.gemm_request(m, m, m, pkg.parse_canonical(g["config"]), reps=10)
+    def shape(key):  # "2048" (square) or "8192x256x8192" (configs[3] non-square)
+        v = [int(t) for t in key.split("x")]
+        return (v[0], v[0], v[0]) if len(v) == 1 else tuple(v)
+
+    for size, g in sorted(table.get("gemm", {}).items(), key=lambda kv: shape(kv[0])):
+        m, n, k = shape(size)
+        flops = 2.0 * m * n * k
+        req = pkg.gemm_request(m, n, k, pkg.parse_canonical(g["config"]), reps=10)
         r = be.evaluate(req)
-        req.repetitions = 30 if m <= 4096 else 10
+        req.repetitions = 30 if flops <= 2.0 * 4096 ** 3 else 10
         rs = sus.evaluate(req)
         if r.ok and rs.ok:
-            gf = 2.0 * m ** 3 / (rs.mean_ms * 1e-3) / 1e9
-            out[f"sgemm_{m}"] = {"config": g["config"], "time_ms": r.time_ms,
-                                 "mean_ms": rs.mean_ms, "gflops": gf,
-                                 "gflops_best": 2.0 * m ** 3 / (r.time_ms * 1e-3) / 1e9,
-                                 "verified": r.verification, "bound": "fp32",
-                                 "frac": gf / fp32_peak, "dram_bytes": g.get("dram_bytes")}
+            gf = flops / (rs.mean_ms * 1e-3) / 1e9
+            out[f"sgemm_{size}"] = {"config": g["config"], "time_ms": r.time_ms,
+                                    "mean_ms": rs.mean_ms, "gflops": gf,
+                                    "gflops_best": flops / (r.time_ms * 1e-3) / 1e9,
+                                    "verified": r.verification, "bound": "fp32",
+                                    "frac": gf / fp32_peak, "dram_bytes": g.get("dram_bytes")}
     for size, t in sorted(table.get("gemm_tf32", {}).items(), key=lambda kv: int(kv[0])):
         m = int(size)
         r = be.evaluate(pkg.gemm_request(m, m, m, pkg.parse_canonical(t["config"]), reps=10,

@@ -143,8 +143,10 @@ int ktc_memset32(ktc_ctx* ctx, ktc_buf dst, uint32_t value, size_t count);
 
 /* One warm-up launch (if warmup > 0; untimed), then `reps` launches, each
  * bracketed by CUDA events on the context's stream and preceded by an L2
- * flush when flush_l2 != 0.  best_ms = min over reps ("best of N",
- * backend.hpp:41-44); all_ms (optional, reps entries) gets every time. */
+ * flush when flush_l2 == 1.  best_ms = min over reps ("best of N",
+ * backend.hpp:41-44); all_ms (optional, reps entries) gets every time.
+ * flush_l2 == 2: the reps launches back to back between one event pair;
+ * best_ms and every all_ms entry = the mean launch duration. */
 int ktc_launch_timed(ktc_ctx* ctx, ktc_fn* fn, const unsigned grid[3], const unsigned block[3],
                      unsigned smem_bytes, void** params, int warmup, int reps, int flush_l2,
                      float* best_ms, float* all_ms);
@@ -236,7 +238,9 @@ typedef struct {
 
 typedef struct {
     int warmup;             /* untimed launches before timing (default 1) */
-    int flush_l2;           /* flush L2 before every timed launch (default 1) */
+    int flush_l2;           /* flush L2 before every timed launch (default 1); 2 = stream
+                             * timing: the repetitions back to back between one event pair,
+                             * time = mean launch duration (no flushes) */
     int verify;             /* device verification of every successful run (default 1) */
     double rel_tol;         /* default 1e-4 (tuner.hpp:148) */
     double abs_tol;         /* default 1e-6 (tuner.hpp:149) */

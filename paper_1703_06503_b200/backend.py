@@ -96,13 +96,16 @@ def gemm_request(m, n, k, cfg: dict, alpha=1.0, beta=0.0, seed=2026, reps=1, tf3
 class CudaBackend:
     def __init__(self, ordinal: int = 0, warmup: int = 1, flush_l2: bool = True,
                  verify: bool = True, rel_tol: float = 1e-4, abs_tol: float = 1e-6,
-                 compile_threads: int = 0, digest_outputs: bool = False, isolate: bool = False):
+                 compile_threads: int = 0, digest_outputs: bool = False, isolate: bool = False,
+                 stream_timing: bool = False):
         """isolate: run every evaluation in a worker process (ktc-worker), so a
-        configuration that faults or hangs costs one runtime_error result."""
+        configuration that faults or hangs costs one runtime_error result.
+        stream_timing: time the repetitions as one back-to-back stream (one
+        event pair, no L2 flushes); time = mean launch duration."""
         self._lib = K.lib()
         o = K.BackendOptions()
         self._lib.ktc_backend_default_options(C.byref(o))
-        o.warmup, o.flush_l2, o.verify = warmup, int(flush_l2), int(verify)
+        o.warmup, o.flush_l2, o.verify = warmup, 2 if stream_timing else int(flush_l2), int(verify)
         o.rel_tol, o.abs_tol, o.compile_threads = rel_tol, abs_tol, compile_threads
         o.digest_outputs = int(digest_outputs)
         o.isolate = int(isolate)

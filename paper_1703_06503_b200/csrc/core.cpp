@@ -631,6 +631,27 @@ int ktc_launch_timed(ktc_ctx* ctx, ktc_fn* fn, const unsigned grid[3], const uns
         rc = launch(ctx, fn->fn, grid[0], grid[1], grid[2], block[0], block[1], block[2],
                     smem_bytes, params);
     if (rc != CUDA_SUCCESS) return fail_cu(ctx, rc, "cuLaunchKernel (warm-up)");
+    if (flush == 2) {
+        // Stream timing: the repetitions back to back between ONE event
+        // pair (no L2 flushes, no events between launches); every
+        // repetition's time is the mean launch duration of the stream.
+        rc = d.cuEventRecord(ctx->events[0], ctx->stream);
+        for (int r = 0; r < reps && rc == CUDA_SUCCESS; ++r)
+            rc = launch(ctx, fn->fn, grid[0], grid[1], grid[2], block[0], block[1], block[2],
+                        smem_bytes, params);
+        if (rc == CUDA_SUCCESS) rc = d.cuEventRecord(ctx->events[1], ctx->stream);
+        if (rc != CUDA_SUCCESS) return fail_cu(ctx, rc, "cuLaunchKernel");
+        rc = wait_event(ctx, ctx->events[1], watchdog_seconds());
+        if (rc != CUDA_SUCCESS) return fail_cu(ctx, rc, "kernel execution");
+        float total = 0.0f;
+        rc = d.cuEventElapsedTime(&total, ctx->events[0], ctx->events[1]);
+        if (rc != CUDA_SUCCESS) return fail_cu(ctx, rc, "cuEventElapsedTime");
+        const float mean = total / float(reps);
+        if (all_ms)
+            for (int r = 0; r < reps; ++r) all_ms[r] = mean;
+        *best_ms = mean;
+        return KTC_OK;
+    }
     for (int r = 0; r < reps; ++r) {
         if (flush) {
             st = flush_l2(ctx);

@@ -282,3 +282,16 @@ def test_parameter_value_errors_match_the_reference(tmp_path, values):
         pkg.Tuner.from_job(text, str(tmp_path)).space_counts()
     want = str(ref_err.value).strip().removeprefix("job file error: ")
     assert want in str(mine_err.value), (str(ref_err.value), str(mine_err.value))
+
+
+def test_tf32_space_counts_follow_the_local_memory_expression():
+    """The TF32 variant's space (BN x BK x STAGES x CG = 48 points) keeps the
+    configurations whose shared memory, STAGES*4*BK*(128 + BN/CG) + 2048
+    bytes (a CTA pair stages half of B per CTA), fits the B200's 232,448 B."""
+    t = pkg.Tuner.gemm(2048, 2048, 2048, tf32=True)
+    want = sum(1 for bn in (64, 128, 256) for bk in (32, 64) for st in (2, 3, 4, 6) for cg in (1, 2)
+               if st * 4 * bk * (128 + bn // cg) + 2048 <= 232448)
+    assert t.space_counts() == (48, 48, want)
+    valid = {t.space_config(i) for i in range(want)}
+    assert "BK=32;BN=256;CG=2;STAGES=6" in valid  # 6 x 32 KiB stages per CTA of a pair
+    assert "BK=32;BN=256;CG=1;STAGES=6" not in valid
