@@ -815,10 +815,12 @@ bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
     p->config.push_back(define("OCC", gemm_occ_policy()));
     p->config.push_back(define("F2", gemm_f2_policy()));
     p->smem = dbuf ? 2 * tile_bytes : tile_bytes;
-    // Compiled in only where the launch policy can split: K >= 2048 (every
-    // split keeps K/s >= 1024) and at most 16 tiles per SM.
+    // Compiled in only where the launch policy can split: K >= 8192 (every
+    // split keeps K/s >= 4096) and at most 16 tiles per SM -- or when a
+    // split count is forced (KTC_GEMM_SPLIT, tests and probes).
     const long long tiles = (I.M / MWG) * (I.N / NWG);
-    if (gemm_tail_policy() && gemm_source().ptx_generator && I.K >= 2048 &&
+    if (gemm_tail_policy() && gemm_source().ptx_generator &&
+        (I.K >= 8192 || std::getenv("KTC_GEMM_SPLIT")) &&
         tiles <= 16LL * be->ctx->limits.sm_count) {
         p->config.push_back(define("TAILK", 1));
         p->tailk = true;
@@ -1109,13 +1111,14 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
             // Split-K launch policy (tools/split_probe.py, DESIGN 4): per-SM
             // balance.  The tiles land ~evenly on the SMs, so a launch of c
             // CTAs per SM runs ceil(c) rounds on the busiest SM; cutting every
-            // tile's K range into s CTAs (each K/s >= 1024) is worth it when
+            // tile's K range into s CTAs (each K/s >= 4096) is worth it when
             // it evens the rounds out by more than the partial-tile reduction
-            // costs (~3%).  8192x256x8192: 3.46 -> 6.92/7 tiles per SM, +12%;
-            // 2048^3 / 4096^3 winners already balanced -> whole tiles.
+            // costs (~3%).  8192x256x8192: 3.46 -> 6.92/7 tiles per SM, +14%;
+            // with K/s = 1024 (2048^3, 64x128 tiles) the same rebalancing
+            // measured 3% slower, so short splits are not offered.
             const unsigned tiles = plan.tiles_x * plan.tiles_y;
             const unsigned sms = unsigned(std::max(ctx->limits.sm_count, 1));
-            const unsigned smax = std::min({8u, plan.ktiles, std::max(unsigned(I.K) / 1024u, 1u)});
+            const unsigned smax = std::min({8u, plan.ktiles, std::max(unsigned(I.K) / 4096u, 1u)});
             unsigned splits = 1;
             double best = -1.0;
             for (unsigned s = 1; s <= smax; ++s) {
