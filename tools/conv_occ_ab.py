@@ -21,10 +21,17 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--filters", default="5,7,9,11")
     ap.add_argument("--n", type=int, default=12)
+    ap.add_argument("--variants", help='e.g. "base:;persist:KTC_CONV_PERSIST=1,KTC_CONV_MINCTA=16"')
     a = ap.parse_args()
+    variants = VARIANTS
+    if a.variants:
+        variants = {}
+        for item in a.variants.split(";"):
+            name, _, envs = item.partition(":")
+            variants[name] = dict(kv.split("=", 1) for kv in envs.split(",") if kv)
     (ROOT / "gpurun_out").mkdir(exist_ok=True)
     res = {}
-    for name, env in VARIANTS.items():
+    for name, env in variants.items():
         out = ROOT / "gpurun_out" / f"conv_occ_{name}.json"
         e = dict(os.environ, **env)
         p = subprocess.run([sys.executable, str(ROOT / "tools" / "conv_sustained_ab.py"), "--out", str(out),
@@ -38,8 +45,9 @@ def main():
             if not r:
                 continue
             ks = [k for k in r if k.startswith(f + "|")]
+            bad = sum(1 for k in ks if r[k][2] != "pass")
             line.append(f"{name}: sus {min(r[k][1] for k in ks) * 1e3:.1f} us, "
-                        f"flushed {min(r[k][0] for k in ks) * 1e3:.1f} us")
+                        f"flushed {min(r[k][0] for k in ks) * 1e3:.1f} us" + (f" ({bad} NOT VERIFIED)" if bad else ""))
         print(" | ".join(line), flush=True)
 
 
