@@ -480,9 +480,10 @@ def main():
         line["configs4_gemm4096"] = gemm_block
     if rank == 0 and args.no_tuned:
         # the roofline always uses the sustained protocol (30 back-to-back
-        # launches, mean): a single flushed launch can end before its output
-        # write-backs drain and read above the copy bandwidth
-        sus = pkg.CudaBackend(devices[0], compile_threads=threads, flush_l2=False, warmup=3)
+        # launches between one event pair, mean launch duration): a single
+        # flushed launch can end before its output write-backs drain and
+        # read above the copy bandwidth
+        sus = pkg.CudaBackend(devices[0], compile_threads=threads, warmup=3, stream_timing=True)
         req = pkg.conv_request(X, Y, F, pkg.parse_canonical(best_row.config), reps=30)
         rs = sus.evaluate(req)
         sus.close()
@@ -491,8 +492,9 @@ def main():
             line["roofline"].update(achieved=gbs, frac=gbs / peaks["hbm_gbs"],
                                     kernel="conv2d_k0 " + best_row.config,
                                     algorithmic_bytes=CONV_BYTES,
-                                    timing="mean of 30 back-to-back launches of this run's best "
-                                           "sampled configuration")
+                                    timing="mean launch duration of 30 back-to-back launches of "
+                                           "this run's best sampled configuration (one CUDA event "
+                                           "pair on the launch stream, no flushes)")
     if rank == 0 and not args.no_tuned:
         line["tuned"] = tuned_block(pkg, devices[0], threads, best_row, peaks)
         best3 = line["tuned"]["conv"].get("3")
@@ -501,7 +503,8 @@ def main():
                 achieved=best3["gbs"], frac=best3["gbs"] / peaks["hbm_gbs"],
                 kernel="conv2d_k0 " + best3["config"], traffic=best3.get("dram_bytes"),
                 algorithmic_bytes=CONV_BYTES,
-                timing="mean of 30 back-to-back launches, CUDA events on the launch stream")
+                timing="mean launch duration of 30 back-to-back launches between one CUDA event "
+                       "pair on the launch stream (no flushes)")
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_configs()
         line["cpu_baseline_kernels"] = cpu_baseline_kernels()
@@ -554,16 +557,18 @@ def tuned_block(pkg, local, threads, sample_best, peaks) -> dict:
     (configs[2]-[4] sizes) and the TF32 variant."""
     table = tuned_table()
     # `be`: the tuner's protocol (L2 flushed, best of 10).  `sus`: 30
-    # back-to-back launches without flushes, mean launch time -- the
+    # back-to-back launches without flushes between one event pair (no events
+    # between launches, tools/launch_overhead_probe.py), mean launch time -- the
     # sustained figure the roofline uses (each launch also pays for the
     # previous launch's L2 write-backs, as in a real pipeline).
     be = pkg.CudaBackend(local, compile_threads=threads)
-    sus = pkg.CudaBackend(local, compile_threads=threads, flush_l2=False, warmup=3)
+    sus = pkg.CudaBackend(local, compile_threads=threads, warmup=3, stream_timing=True)
     fp32_peak = fp32_peak_gflops()
     tf32_peak = tf32_peak_gflops()
     out = {"conv": {}, "source": "tuned/b200_winners.json" if table else "this run's sample",
-           "timing": "time_ms: best of 10 flushed launches; mean_ms: mean of 30 back-to-back "
-                     "launches (roofline uses mean_ms)"}
+           "timing": "time_ms: best of 10 flushed launches; mean_ms: mean launch duration of 30 "
+                     "back-to-back launches between one event pair, no flushes (roofline uses "
+                     "mean_ms)"}
     for f in (3, 5, 7, 9, 11):
         entry = table.get("conv", {}).get(str(f))
         cfg = entry["config"] if entry else (sample_best.config if f == 3 else None)
@@ -609,13 +614,17 @@ def tuned_block(pkg, local, threads, sample_best, peaks) -> dict:
                                     "frac": gf / fp32_peak, "dram_bytes": g.get("dram_bytes")}
     for size, t in sorted(table.get("gemm_tf32", {}).items(), key=lambda kv: int(kv[0])):
         m = int(size)
-        r = be.evaluate(pkg.gemm_request(m, m, m, pkg.parse_canonical(t["config"]), reps=10,
-                                         tf32=True))
-        if r.ok:
-            tf = 2.0 * m ** 3 / (r.time_ms * 1e-3) / 1e9
-            out[f"tf32_{m}"] = {"config": t["config"], "time_ms": r.time_ms, "gflops": tf,
+        req = pkg.gemm_request(m, m, m, pkg.parse_canonical(t["config"]), reps=10, tf32=True)
+        r = be.evaluate(req)
+        req.repetitions = 30 if m <= 4096 else 10
+        rs = sus.evaluate(req)
+        if r.ok and rs.ok:
+            tf = 2.0 * m ** 3 / (rs.mean_ms * 1e-3) / 1e9
+            out[f"tf32_{m}"] = {"config": t["config"], "time_ms": r.time_ms, "mean_ms": rs.mean_ms,
+                                "gflops": tf, "gflops_best": 2.0 * m ** 3 / (r.time_ms * 1e-3) / 1e9,
                                 "verified": r.verification, "tolerance": "rel 1e-3, abs 1e-6",
-                                "bound": "tensor (tf32)", "frac": tf / tf32_peak}
+                                "bound": "tensor (tf32)", "frac": tf / tf32_peak,
+                                "dram_bytes": t.get("dram_bytes")}
     out["fp32_peak_gflops"] = fp32_peak
     out["tf32_peak_gflops"] = tf32_peak
     out["tf32_peak_src"] = ("half of MEASURED_PEAKS.json bf16_tflops (dense bf16 burst, cuBLAS); "
