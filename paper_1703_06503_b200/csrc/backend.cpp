@@ -86,7 +86,6 @@ struct Plan {
     double compile_cost = 1.0;  // relative NVRTC cost estimate (CompileService ordering)
     // SGEMM TAILK: 1-D grid of whole tiles + K-split tail tiles (ptxgen_gemm.cpp)
     bool tailk = false;
-    bool persist = false;  // conv PERSIST: grid = resident CTAs walking the tiles
     unsigned tiles_x = 0, tiles_y = 0, ktiles = 0, tile_floats = 0;
 };
 
@@ -620,18 +619,6 @@ const char* conv_trace_dir() {
     return v && *v ? v : nullptr;
 }
 
-// Persistent LOCAL = 2 conv CTAs (ptxgen_conv PERSIST): one launch of
-// occupancy x SMs CTAs, each walking tiles ctaid + k * nctaid with its halo
-// barrier reused and the next tile's TMA in flight during the epilogue.
-// KTC_CONV_PERSIST=1 enables it.
-int conv_persist_policy() {
-    static const int v = [] {
-        const char* e = std::getenv("KTC_CONV_PERSIST");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-
 // Conv register budget (ptxgen_conv MINCTA -> .minnctapersm): 0 = ptxas's
 // own choice, 1 = the shared-memory-limited CTA count, n > 1 = n CTAs per
 // SM.  KTC_CONV_MINCTA overrides.
@@ -712,10 +699,6 @@ bool plan_conv(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
         if (n > 1) o.push_back(define("MINCTA", n));
     }
     if (conv_trace_dir()) o.push_back(define("TRACE", 1));
-    if (LOCAL == 2 && conv_persist_policy()) {
-        o.push_back(define("PERSIST", 1));
-        p->persist = true;
-    }
     p->compile_cost = unrolled_cost(double(XWPT * YWPT) * (UNR ? double(I.F) * I.F : 4.0));
     if (p->smem > be->ctx->limits.smem_per_block_optin) {
         *why = "needs " + std::to_string(p->smem) + " bytes of shared memory; the device allows " +
@@ -1084,16 +1067,6 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
         iP = I.ipitch;
         pOut = I.out[0];
         params = {&iX, &iY, &fW, &pImg, &iP, &pOut, &tmap};
-        if (plan.persist) {
-            int occ = 0;
-            d.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn->fn,
-                                                          int(plan.block[0] * plan.block[1]),
-                                                          size_t(plan.smem));
-            const unsigned tiles = plan.grid[0] * plan.grid[1];
-            const unsigned slots = unsigned(std::max(occ, 1)) * unsigned(ctx->limits.sm_count);
-            plan.grid[0] = std::min(tiles, slots);
-            plan.grid[1] = 1;
-        }
         if (conv_trace_dir()) {
             const size_t tb = size_t(plan.grid[0]) * plan.grid[1] * 32;
             if (d.cuMemAlloc(&trace_buf, tb) != CUDA_SUCCESS) {

@@ -22,7 +22,6 @@
 //   UNR = 0    rolled tap loops (runtime tap index into c_taps)
 //   epilogue   out = W * acc, vector stores, GUARD predicates for ragged tiles
 #include <algorithm>
-#include <functional>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -36,7 +35,7 @@ namespace {
 
 struct ConvGen {
     int FS = 0, XWG = 0, YWG = 0, XWPT = 0, YWPT = 0, LOCAL = 0, VW = 1, PAD = 0, UNR = 1;
-    int GUARD = 0, OUT_VEC = 1, CF2 = 1, MINCTA = 1, TRACE = 0, PERSIST = 0;
+    int GUARD = 0, OUT_VEC = 1, CF2 = 1, MINCTA = 1, TRACE = 0;
     int SP = 0, PWO = 0, BW = 0, BH = 0, NB = 0, NP = 0, PF = 0;
 };
 
@@ -64,8 +63,6 @@ ConvGen parse(const Defines& problem, const Defines& c) {
     g.CF2 = int(def_value(c, "CF2", false, 1));
     g.MINCTA = int(def_value(c, "MINCTA", false, 1));
     g.TRACE = int(def_value(c, "TRACE", false, 0));
-    g.PERSIST = g.LOCAL == 2 ? int(def_value(c, "PERSIST", false, 0)) : 0;
-    if (g.PERSIST) g.TRACE = 0;
     if (g.LOCAL == 1) g.SP = int(def_value(c, "SP", true));
     if (g.LOCAL == 2) {
         g.PWO = int(def_value(c, "PWO", true));
@@ -174,35 +171,8 @@ std::string emit_entry(const ConvGen& g, const std::string& name) {
         x.op("mov.u64 " + trace_t0 + ", %globaltimer");
         (void)o;
     }
-    // PERSIST (host switch, LOCAL = 2): a grid of resident CTAs walks the
-    // tiles tile = ctaid.x + k * nctaid.x; x0 / y0 are set per tile below.
-    std::string tile, ntiles, gxr, kpar;
-    if (g.PERSIST) {
-        tile = x.r();
-        ntiles = x.r();
-        gxr = x.r();
-        kpar = x.r();
-        const std::string gy = x.r();
-        x.op("add.u32 " + gxr + ", " + rX + ", " + imm(TX - 1));
-        x.op("shr.u32 " + gxr + ", " + gxr + ", " + imm(log2i(TX)));
-        x.op("add.u32 " + gy + ", " + rY + ", " + imm(TY - 1));
-        x.op("shr.u32 " + gy + ", " + gy + ", " + imm(log2i(TY)));
-        x.op("mul.lo.u32 " + ntiles + ", " + gxr + ", " + gy);
-        x.op("mov.u32 " + tile + ", " + cx);
-        x.op("mov.u32 " + kpar + ", 0");
-    } else {
-        x.op("mul.lo.u32 " + x0 + ", " + cx + ", " + imm(TX));
-        x.op("mul.lo.u32 " + y0 + ", " + cy + ", " + imm(TY));
-    }
-    // Tile origin of tile index t (PERSIST).
-    auto tile_origin = [&](const std::string& t, const std::string& ox, const std::string& oy) {
-        const std::string q = x.r(), r = x.r();
-        x.op("div.u32 " + q + ", " + t + ", " + gxr);
-        x.op("mul.lo.u32 " + r + ", " + q + ", " + gxr);
-        x.op("sub.u32 " + r + ", " + t + ", " + r);
-        x.op("mul.lo.u32 " + ox + ", " + r + ", " + imm(TX));
-        x.op("mul.lo.u32 " + oy + ", " + q + ", " + imm(TY));
-    };
+    x.op("mul.lo.u32 " + x0 + ", " + cx + ", " + imm(TX));
+    x.op("mul.lo.u32 " + y0 + ", " + cy + ", " + imm(TY));
     // Column of group gi (floats, relative to the tile): (gi*XWG + tx) * VW.
     std::vector<std::string> colf(static_cast<size_t>(NG));  // u32 float index
     for (int gi = 0; gi < NG; ++gi) {
@@ -211,9 +181,6 @@ std::string emit_entry(const ConvGen& g, const std::string& name) {
              imm(gi * g.XWG * g.VW));
     }
 
-    // PERSIST plumbing filled in by the LOCAL = 2 staging.
-    std::string persist_bar, persist_top, persist_exit, lead_not;
-    std::function<void(const std::string&, const std::string&)> issue_halo;
     // ---- staging: row base addresses and column byte offsets
     const char* space = g.LOCAL == 0 ? "global.nc" : "shared";
     std::vector<std::string> colb(static_cast<size_t>(NG));  // byte offset of the group's window start
@@ -333,60 +300,35 @@ std::string emit_entry(const ConvGen& g, const std::string& name) {
     } else if (g.LOCAL == 2) {
         const std::string bar = x.r();
         x.op("add.u32 " + bar + ", " + sbase + ", " + imm((long long)g.NP * g.PF * 4));
-        persist_bar = bar;
         const std::string pz = x.p(), t = x.r(), after = x.label();
         x.op("or.b32 " + t + ", " + tx + ", " + ty);
         x.op("setp.ne.u32 " + pz + ", " + t + ", 0");
-        lead_not = pz;
-        const std::string tm = x.d();
-        x.op("mov.b64 " + tm + ", " + P + "6");
-        x.op("cvta.param.u64 " + tm + ", " + tm);
-        // One thread: arm the barrier with the halo bytes, issue the boxes.
-        issue_halo = [&, tm, bar](const std::string& ox, const std::string& oy) {
-            const std::string bytes = x.r();
-            x.op("mov.u32 " + bytes + ", " + imm((long long)g.NP * g.NB * g.BW * g.BH * 4));
-            x.op("mbarrier.arrive.expect_tx.shared::cta.b64 _, [" + bar + "], " + bytes);
-            for (int pnl = 0; pnl < g.NP; ++pnl)
-                for (int b = 0; b < g.NB; ++b) {
-                    const std::string dst = x.r(), xc = x.r(), yc = x.r();
-                    x.op("add.u32 " + dst + ", " + sbase + ", " +
-                         imm(((long long)pnl * g.PF + (long long)b * g.BH * g.BW) * 4));
-                    x.op("add.u32 " + xc + ", " + ox + ", " + imm((long long)pnl * g.PWO));
-                    x.op("add.u32 " + yc + ", " + oy + ", " + imm((long long)b * g.BH));
-                    x.op("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [" +
-                         dst + "], [" + tm + ", {" + xc + ", " + yc + "}], [" + bar + "]");
-                }
-        };
         x.op("@" + pz + " bra " + after);
         x.op("mbarrier.init.shared::cta.b64 [" + bar + "], 1");
         x.op("fence.mbarrier_init.release.cluster");
-        if (g.PERSIST) {
-            const std::string pt = x.p(), ox = x.r(), oy = x.r();
-            x.op("setp.ge.u32 " + pt + ", " + tile + ", " + ntiles);
-            x.op("@" + pt + " bra " + after);
-            tile_origin(tile, ox, oy);
-            issue_halo(ox, oy);
-        } else {
-            issue_halo(x0, y0);
-        }
+        const std::string bytes = x.r();
+        x.op("mov.u32 " + bytes + ", " + imm((long long)g.NP * g.NB * g.BW * g.BH * 4));
+        x.op("mbarrier.arrive.expect_tx.shared::cta.b64 _, [" + bar + "], " + bytes);
+        const std::string tm = x.d();
+        x.op("mov.b64 " + tm + ", " + P + "6");
+        x.op("cvta.param.u64 " + tm + ", " + tm);
+        for (int pnl = 0; pnl < g.NP; ++pnl)
+            for (int b = 0; b < g.NB; ++b) {
+                const std::string dst = x.r(), xc = x.r(), yc = x.r();
+                x.op("add.u32 " + dst + ", " + sbase + ", " +
+                     imm(((long long)pnl * g.PF + (long long)b * g.BH * g.BW) * 4));
+                x.op("add.u32 " + xc + ", " + x0 + ", " + imm((long long)pnl * g.PWO));
+                x.op("add.u32 " + yc + ", " + y0 + ", " + imm((long long)b * g.BH));
+                x.op("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [" +
+                     dst + "], [" + tm + ", {" + xc + ", " + yc + "}], [" + bar + "]");
+            }
         x.lab(after);
         x.op("bar.sync 0");
-        if (g.PERSIST) {
-            // ---- tile loop: every tile of this CTA reuses the barrier (phase kpar)
-            persist_top = x.label();
-            persist_exit = x.label();
-            const std::string pt = x.p();
-            x.lab(persist_top);
-            x.op("setp.ge.u32 " + pt + ", " + tile + ", " + ntiles);
-            x.op("@" + pt + " bra " + persist_exit);
-            tile_origin(tile, x0, y0);
-        }
         // Bounded wait (a lost transaction traps -> runtime_error, never a hang).
         const std::string spin = x.d(), lw = x.label(), ld = x.label(), pd = x.p(), pc = x.p();
         x.op("mov.u64 " + spin + ", 0");
         x.lab(lw);
-        x.op("mbarrier.try_wait.parity.shared::cta.b64 " + pd + ", [" + bar + "], " +
-             (g.PERSIST ? kpar : std::string("0")));
+        x.op("mbarrier.try_wait.parity.shared::cta.b64 " + pd + ", [" + bar + "], 0");
         x.op("@" + pd + " bra " + ld);
         x.op("add.u64 " + spin + ", " + spin + ", 1");
         x.op("setp.lt.u64 " + pc + ", " + spin + ", " + imm(1ll << 26));
@@ -544,21 +486,6 @@ std::string emit_entry(const ConvGen& g, const std::string& name) {
         x.op("@" + pj + " bra " + ljj);
     }
 
-    std::string next_tile;
-    if (g.PERSIST) {
-        // The halo tile is consumed: the next tile's TMA flies during the epilogue.
-        next_tile = x.r();
-        const std::string nct = x.r(), skip = x.label(), pn = x.p(), ox = x.r(), oy = x.r();
-        x.op("bar.sync 0");
-        x.op("mov.u32 " + nct + ", %nctaid.x");
-        x.op("add.u32 " + next_tile + ", " + tile + ", " + nct);
-        x.op("@" + lead_not + " bra " + skip);
-        x.op("setp.ge.u32 " + pn + ", " + next_tile + ", " + ntiles);
-        x.op("@" + pn + " bra " + skip);
-        tile_origin(next_tile, ox, oy);
-        issue_halo(ox, oy);
-        x.lab(skip);
-    }
     // ---- epilogue: out = W * acc
     for (int j = 0; j < g.YWPT; ++j) {
         const std::string row = x.r(), next = x.label();
@@ -622,12 +549,6 @@ std::string emit_entry(const ConvGen& g, const std::string& name) {
             x.lab(gdone);
         }
         x.lab(next);
-    }
-    if (g.PERSIST) {
-        x.op("mov.u32 " + tile + ", " + next_tile);
-        x.op("xor.b32 " + kpar + ", " + kpar + ", 1");
-        x.op("bra.uni " + persist_top);
-        x.lab(persist_exit);
     }
     if (g.TRACE) {
         const std::string t1 = x.d(), sm = x.r(), sm64 = x.d();

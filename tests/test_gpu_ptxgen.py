@@ -71,3 +71,4 @@ def test_ptx_codegen_matches_nvrtc_bit_for_bit():
     assert not bad, bad[:5]
     assert sum(1 for k, v in gen.items() if v[0] == "ok" and not k.startswith("gemm")) > 100
     assert sum(1 for k, v in gen.items() if v[0] == "ok" and k.startswith("gemm")) > 50
+
