@@ -28,10 +28,10 @@ def main():
             f = int(w[4:])
             cfg = table["conv"][str(f)]["config"]
             r = be.evaluate(pkg.conv_request(8192, 4096, f, pkg.parse_canonical(cfg), reps=2))
-        elif w.startswith("gemm:"):  # gemm:<size>:<canonical config>
+        elif w.startswith("gemm:"):  # gemm:<size or MxNxK>:<canonical config>
             _, size, cfg = w.split(":", 2)
-            m = int(size)
-            r = be.evaluate(pkg.gemm_request(m, m, m, pkg.parse_canonical(cfg), reps=2))
+            m, n, k = (int(size),) * 3 if "x" not in size else (int(v) for v in size.split("x"))
+            r = be.evaluate(pkg.gemm_request(m, n, k, pkg.parse_canonical(cfg), reps=2))
         elif w.startswith("tf32:"):  # tf32:<size>:<canonical config>
             _, size, cfg = w.split(":", 2)
             m = int(size)
