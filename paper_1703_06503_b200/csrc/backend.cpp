@@ -86,6 +86,7 @@ struct Plan {
     double compile_cost = 1.0;  // relative NVRTC cost estimate (CompileService ordering)
     // SGEMM TAILK: 1-D grid of whole tiles + K-split tail tiles (ptxgen_gemm.cpp)
     bool tailk = false;
+    bool sk = false;  // SGEMM stream-K (ptxgen_gemm SK)
     unsigned tiles_x = 0, tiles_y = 0, ktiles = 0, tile_floats = 0;
 };
 
@@ -754,6 +755,16 @@ int gemm_tail_policy() {
     return v;
 }
 
+// Stream-K for unevenly distributed SGEMM tiles (ptxgen_gemm SK);
+// KTC_GEMM_SK=0 disables it.
+int gemm_sk_policy() {
+    static const int v = [] {
+        const char* e = std::getenv("KTC_GEMM_SK");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 // Packed FFMA2 outer products (gemm.cu F2); KTC_GEMM_F2 overrides.
 int gemm_f2_policy() {
     static const int v = [] {
@@ -819,11 +830,23 @@ bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
     // split keeps K/s >= 4096) and at most 16 tiles per SM -- or when a
     // split count is forced (KTC_GEMM_SPLIT, tests and probes).
     const long long tiles = (I.M / MWG) * (I.N / NWG);
-    if (gemm_tail_policy() && gemm_source().ptx_generator &&
-        (I.K >= 8192 || std::getenv("KTC_GEMM_SPLIT")) &&
-        tiles <= 16LL * be->ctx->limits.sm_count) {
+    // Stream-K (SK) where whole tiles land unevenly on the SMs: the busiest
+    // SM runs ceil(c) tiles for c = tiles / SMs on average; below 92% balance
+    // (and with at least 8 K-tiles to deal) the units are dealt evenly.
+    const double per_sm = double(tiles) / double(std::max(be->ctx->limits.sm_count, 1));
+    const bool sk = gemm_sk_policy() && gemm_source().ptx_generator && !std::getenv("KTC_GEMM_SPLIT") &&
+                    I.K / KWG >= 8 && tiles <= 16LL * be->ctx->limits.sm_count &&
+                    per_sm / std::ceil(per_sm) < 0.92;
+    if (sk) {
+        p->config.push_back(define("SK", 1));
+        p->sk = true;
+    } else if (gemm_tail_policy() && gemm_source().ptx_generator &&
+               (I.K >= 8192 || std::getenv("KTC_GEMM_SPLIT")) &&
+               tiles <= 16LL * be->ctx->limits.sm_count) {
         p->config.push_back(define("TAILK", 1));
         p->tailk = true;
+    }
+    if (p->sk || p->tailk) {
         p->smem += 16;  // the arrival flag after the staged tiles
         p->tiles_x = unsigned(I.M / MWG);
         p->tiles_y = unsigned(I.N / NWG);
@@ -1107,6 +1130,55 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
         pC = I.dev[7];
         pOut = I.out[0];
         params = {&iM, &iN, &iK, &fA, &fB, &pA, &pB, &pC, &pOut};
+        if (plan.sk) {
+            // Stream-K: G = resident CTAs (occupancy x SMs) share the
+            // tiles x K-tiles units evenly; MAXSEG = most segments of a tile.
+            int occ = 0;
+            d.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn->fn,
+                                                          int(plan.block[0] * plan.block[1]),
+                                                          size_t(plan.smem));
+            const unsigned tiles = plan.tiles_x * plan.tiles_y;
+            const unsigned long long U = (unsigned long long)tiles * plan.ktiles;
+            const unsigned G = unsigned(std::min<unsigned long long>(
+                U, (unsigned long long)std::max(occ, 1) * unsigned(ctx->limits.sm_count)));
+            auto cv = [&](unsigned long long v) { return ((v + 1) * G - 1) / U; };
+            unsigned maxseg = 1;
+            for (unsigned t = 0; t < tiles; ++t)
+                maxseg = std::max(maxseg, unsigned(cv((unsigned long long)(t + 1) * plan.ktiles - 1) -
+                                                   cv((unsigned long long)t * plan.ktiles) + 1));
+            const size_t ws = size_t(tiles) * maxseg * plan.tile_floats * 4;
+            const size_t cn = size_t(tiles) * 4;
+            if (ws > be->tail_ws_bytes) {
+                if (be->tail_ws) d.cuMemFree(be->tail_ws);
+                be->tail_ws = 0;
+                be->tail_ws_bytes = 0;
+                if (d.cuMemAlloc(&be->tail_ws, ws) != CUDA_SUCCESS) {
+                    set_msg(out, "cannot allocate the stream-K workspace");
+                    return KTC_OK;
+                }
+                be->tail_ws_bytes = ws;
+            }
+            if (cn > be->tail_cnt_bytes) {
+                if (be->tail_cnt) d.cuMemFree(be->tail_cnt);
+                be->tail_cnt = 0;
+                be->tail_cnt_bytes = 0;
+                if (d.cuMemAlloc(&be->tail_cnt, cn) != CUDA_SUCCESS ||
+                    d.cuMemsetD32Async(be->tail_cnt, 0, cn / 4, ctx->stream) != CUDA_SUCCESS) {
+                    set_msg(out, "cannot allocate the stream-K counters");
+                    return KTC_OK;
+                }
+                be->tail_cnt_bytes = cn;
+            }
+            tk_ws = be->tail_ws;
+            tk_cnt = be->tail_cnt;
+            tk_full = unsigned(U);   // SK: p11 = units, p12 = MAXSEG, p13 = tiles_x, p14 = K-tiles
+            tk_splits = maxseg;
+            tk_gx = plan.tiles_x;
+            tk_kt = plan.ktiles;
+            params.insert(params.end(), {&tk_ws, &tk_cnt, &tk_full, &tk_splits, &tk_gx, &tk_kt});
+            plan.grid[0] = G;
+            plan.grid[1] = 1;
+        }
         if (plan.tailk) {
             // Split-K launch policy (tools/split_probe.py, DESIGN 4): per-SM
             // balance.  The tiles land ~evenly on the SMs, so a launch of c

@@ -40,7 +40,7 @@ long long dv(const Defines& ds, const char* name, bool required, long long fallb
 
 struct GemmGen {
     int MWG, NWG, KWG, MDIMC, NDIMC, SA, SB, MDIMA, NDIMB, STRM, STRN, VWM, VWN, KWI;
-    int DBUF, OCC, F2, TAILK;
+    int DBUF, OCC, F2, TAILK, SK;
 };
 
 GemmGen parse(const Defines& c) {
@@ -63,6 +63,7 @@ GemmGen parse(const Defines& c) {
     g.OCC = int(dv(c, "OCC", false, 0));
     g.F2 = int(dv(c, "F2", false, 1));
     g.TAILK = int(dv(c, "TAILK", false, 0));
+    g.SK = g.TAILK ? 0 : int(dv(c, "SK", false, 0));
     return g;
 }
 
@@ -191,6 +192,8 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
     // partial tile, and the last of a tile's splits to arrive (counter)
     // reduces the partials in split order and runs the epilogue.
     std::string dW, dCnt, rFull, rSplits, pnorm, tail_t, split;
+    std::string sk_u, sk_u1, sk_tile, sk_kt0, sk_kt1, sk_j, sk_nseg, sk_maxseg, sk_top, sk_next,
+        sk_exit;
     if (g.TAILK) {
         dW = x.d();
         dCnt = x.d();
@@ -227,6 +230,93 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
         x.op("mul.lo.u32 " + kt1 + ", " + kt1 + ", " + imm(g.KWG));
         x.op("selp.u32 " + kbeg + ", 0, " + kt0 + ", " + pnorm);
         x.op("selp.u32 " + kend + ", " + rK + ", " + kt1 + ", " + pnorm);
+    } else if (g.SK) {
+        // SK (host switch, part of the compile key): stream-K.  The
+        // tiles x K-tiles units are dealt to the 1-D grid of G CTAs as
+        // contiguous ranges [c*U/G, (c+1)*U/G); a CTA walks its range as
+        // segments (one per tile it touches).  A segment that is a whole
+        // tile runs the epilogue; otherwise it stores its partial tile in
+        // slot tile*MAXSEG + j (j = its index among the tile's segments) and
+        // the last of the tile's segments to arrive sums the partials in
+        // segment order (deterministic) and runs the epilogue.
+        dW = x.d();
+        dCnt = x.d();
+        const std::string rU = x.r(), rGX = x.r(), rKT = x.r(), rG = x.r(), c = x.r(), t = x.d();
+        sk_maxseg = x.r();
+        x.op("ld.param.u64 " + dW + ", [" + P + "9]");
+        x.op("ld.param.u64 " + dCnt + ", [" + P + "10]");
+        x.op("ld.param.u32 " + rU + ", [" + P + "11]");
+        x.op("ld.param.u32 " + sk_maxseg + ", [" + P + "12]");
+        x.op("ld.param.u32 " + rGX + ", [" + P + "13]");
+        x.op("ld.param.u32 " + rKT + ", [" + P + "14]");
+        x.op("cvta.to.global.u64 " + dW + ", " + dW);
+        x.op("cvta.to.global.u64 " + dCnt + ", " + dCnt);
+        x.op("mov.u32 " + c + ", %ctaid.x");
+        x.op("mov.u32 " + rG + ", %nctaid.x");
+        sk_u = x.r();
+        sk_u1 = x.r();
+        // u0(c) = floor(c * U / G)
+        auto u0 = [&](const std::string& cc, const std::string& out) {
+            x.op("mul.wide.u32 " + t + ", " + cc + ", " + rU);
+            const std::string gd = x.d();
+            x.op("cvt.u64.u32 " + gd + ", " + rG);
+            x.op("div.u64 " + t + ", " + t + ", " + gd);
+            x.op("cvt.u32.u64 " + out + ", " + t);
+        };
+        // cv(v) = the CTA whose range holds unit v = floor(((v+1)*G - 1) / U)
+        auto cv = [&](const std::string& v, const std::string& out) {
+            const std::string v1 = x.r(), ud = x.d();
+            x.op("add.u32 " + v1 + ", " + v + ", 1");
+            x.op("mul.wide.u32 " + t + ", " + v1 + ", " + rG);
+            x.op("sub.u64 " + t + ", " + t + ", 1");
+            x.op("cvt.u64.u32 " + ud + ", " + rU);
+            x.op("div.u64 " + t + ", " + t + ", " + ud);
+            x.op("cvt.u32.u64 " + out + ", " + t);
+        };
+        u0(c, sk_u);
+        {
+            const std::string c1 = x.r();
+            x.op("add.u32 " + c1 + ", " + c + ", 1");
+            u0(c1, sk_u1);
+        }
+        sk_top = x.label();
+        sk_next = x.label();
+        sk_exit = x.label();
+        x.lab(sk_top);
+        {
+            const std::string pe = x.p();
+            x.op("setp.ge.u32 " + pe + ", " + sk_u + ", " + sk_u1);
+            x.op("@" + pe + " bra " + sk_exit);
+        }
+        x.op("bar.sync 0");  // the previous segment is done with the staged tiles
+        sk_tile = x.r();
+        sk_kt0 = x.r();
+        sk_kt1 = x.r();
+        sk_j = x.r();
+        sk_nseg = x.r();
+        pnorm = x.p();
+        const std::string rest = x.r(), first = x.r(), last = x.r(), v = x.r();
+        x.op("div.u32 " + sk_tile + ", " + sk_u + ", " + rKT);
+        x.op("mul.lo.u32 " + v + ", " + sk_tile + ", " + rKT);
+        x.op("sub.u32 " + sk_kt0 + ", " + sk_u + ", " + v);
+        x.op("sub.u32 " + rest + ", " + sk_u1 + ", " + sk_u);
+        x.op("add.u32 " + sk_kt1 + ", " + sk_kt0 + ", " + rest);
+        x.op("min.u32 " + sk_kt1 + ", " + sk_kt1 + ", " + rKT);
+        cv(v, first);  // v = tile * KT
+        {
+            const std::string vl = x.r();
+            x.op("add.u32 " + vl + ", " + v + ", " + rKT);
+            x.op("sub.u32 " + vl + ", " + vl + ", 1");
+            cv(vl, last);
+        }
+        x.op("sub.u32 " + sk_j + ", " + c + ", " + first);
+        x.op("sub.u32 " + sk_nseg + ", " + last + ", " + first);
+        x.op("add.u32 " + sk_nseg + ", " + sk_nseg + ", 1");
+        x.op("setp.eq.u32 " + pnorm + ", " + sk_nseg + ", 1");
+        x.op("rem.u32 " + cx + ", " + sk_tile + ", " + rGX);
+        x.op("div.u32 " + cy + ", " + sk_tile + ", " + rGX);
+        x.op("mul.lo.u32 " + kbeg + ", " + sk_kt0 + ", " + imm(g.KWG));
+        x.op("mul.lo.u32 " + kend + ", " + sk_kt1 + ", " + imm(g.KWG));
     } else {
         x.op("mov.u32 " + cx + ", %ctaid.x");
         x.op("mov.u32 " + cy + ", %ctaid.y");
@@ -572,18 +662,26 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
     x.op("@" + pmore + " bra " + lk0);
     x.lab(lend);
 
-    // ---- TAILK: partial tiles of the tail wave meet here
-    if (g.TAILK) {
+    // ---- TAILK / SK: partial tiles meet here
+    if (g.TAILK || g.SK) {
         const std::string lepi = x.label();
         x.op("@" + pnorm + " bra " + lepi);
         const long long tile_bytes = (long long)g.MWG * g.NWG * 4;
-        // this CTA's partial: W + ((tail_t * s + split) * tile_bytes)
+        // this CTA's partial: W + (slot * tile_bytes); the tile's partials
+        // start at slot tslot; cidx = the tile's arrival counter; nparts
+        // partials are summed by the last to arrive.
         const std::string slot = x.r(), wmine = x.d(), wtile = x.d(), tmp = x.d();
-        x.op("mad.lo.u32 " + slot + ", " + tail_t + ", " + rSplits + ", " + split);
+        const std::string tslot = x.r(), cidx = g.SK ? sk_tile : tail_t,
+                          nparts = g.SK ? sk_nseg : rSplits;
+        if (g.SK) {
+            x.op("mul.lo.u32 " + tslot + ", " + sk_tile + ", " + sk_maxseg);
+            x.op("add.u32 " + slot + ", " + tslot + ", " + sk_j);
+        } else {
+            x.op("mad.lo.u32 " + slot + ", " + tail_t + ", " + rSplits + ", " + split);
+            x.op("mul.lo.u32 " + tslot + ", " + tail_t + ", " + rSplits);
+        }
         x.op("mul.wide.u32 " + tmp + ", " + slot + ", " + imm(tile_bytes));
         x.op("add.u64 " + wmine + ", " + dW + ", " + tmp);
-        const std::string tslot = x.r();
-        x.op("mul.lo.u32 " + tslot + ", " + tail_t + ", " + rSplits);
         x.op("mul.wide.u32 " + tmp + ", " + tslot + ", " + imm(tile_bytes));
         x.op("add.u64 " + wtile + ", " + dW + ", " + tmp);
         // byte offset of (mi, e, ni) inside a tile: same element map as the epilogue
@@ -618,7 +716,7 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
             x.op("cvt.u32.u64 " + flag + ", " + d);
             x.op("add.u32 " + flag + ", " + flag + ", " + imm(flag_off));
         }
-        x.op("mul.wide.u32 " + cnt_a + ", " + tail_t + ", 4");
+        x.op("mul.wide.u32 " + cnt_a + ", " + cidx + ", 4");
         x.op("add.u64 " + cnt_a + ", " + dCnt + ", " + cnt_a);
         x.op("setp.eq.u32 " + ptid0 + ", " + tid + ", 0");
         {
@@ -632,9 +730,10 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
         {
             const std::string seen = x.r(), last = x.r(), plast = x.p();
             x.op("ld.shared.u32 " + seen + ", [" + flag + "]");
-            x.op("sub.u32 " + last + ", " + rSplits + ", 1");
+            x.op("sub.u32 " + last + ", " + nparts + ", 1");
             x.op("setp.ne.u32 " + plast + ", " + seen + ", " + last);
-            x.op("@" + plast + " ret");  // not the last split of this tile
+            if (g.SK) x.op("@" + plast + " bra " + sk_next);  // another segment sums this tile
+            else x.op("@" + plast + " ret");  // not the last split of this tile
         }
         x.op("fence.acq_rel.gpu");
         {
@@ -674,7 +773,7 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
         }
         x.op("add.u64 " + wj + ", " + wj + ", " + imm(tile_bytes));
         x.op("add.u32 " + j + ", " + j + ", 1");
-        x.op("setp.lt.u32 " + pj + ", " + j + ", " + rSplits);
+        x.op("setp.lt.u32 " + pj + ", " + j + ", " + nparts);
         x.op("@" + pj + " bra " + lj);
         x.lab(lepi);
     }
@@ -728,6 +827,14 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
             }
         }
     }
+    if (g.SK) {
+        x.lab(sk_next);
+        const std::string dk = x.r();
+        x.op("sub.u32 " + dk + ", " + sk_kt1 + ", " + sk_kt0);
+        x.op("add.u32 " + sk_u + ", " + sk_u + ", " + dk);
+        x.op("bra.uni " + sk_top);
+        x.lab(sk_exit);
+    }
     x.op("ret");
 
     std::ostringstream e;
@@ -736,7 +843,7 @@ std::string emit_entry(const GemmGen& g, const std::string& name) {
       << "2,\n\t.param .f32 " << P << "3,\n\t.param .f32 " << P << "4,\n\t.param .u64 .ptr .align 1 "
       << P << "5,\n\t.param .u64 .ptr .align 1 " << P << "6,\n\t.param .u64 .ptr .align 1 " << P
       << "7,\n\t.param .u64 .ptr .align 1 " << P << "8";
-    if (g.TAILK)
+    if (g.TAILK || g.SK)
         e << ",\n\t.param .u64 .ptr .align 1 " << P << "9,\n\t.param .u64 .ptr .align 1 " << P
           << "10,\n\t.param .u32 " << P << "11,\n\t.param .u32 " << P << "12,\n\t.param .u32 " << P
           << "13,\n\t.param .u32 " << P << "14";
