@@ -194,7 +194,18 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const u32 rank = CG == 2 ? cluster_rank() : 0u;
-    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    // Grouped rasterisation: clusters are launched x-fastest; tile (mp, np)
+    // of the pid-th cluster walks GROUP_M tile-rows per column so that the
+    // clusters resident at one time share A rows and B columns in L2 (at
+    // 8192^3 the plain order re-read A from DRAM about once per wave).
+    const int GROUP_M = 8;
+    const int nmp = gridDim.x / CG;  // tile-rows (CTA pairs for CG = 2)
+    const int pid = blockIdx.y * nmp + blockIdx.x / CG;
+    const int span = GROUP_M * gridDim.y;
+    const int first = (pid / span) * GROUP_M;
+    const int rows = min(nmp - first, GROUP_M);
+    const int mp = first + (pid % span) % rows, np = (pid % span) / rows;
+    const int m0 = (mp * CG + (int)rank) * BM, n0 = np * BN;
     const int kblocks = K / BK;
     const u32 full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES),
               accb = smem_u32(bars + 2 * STAGES);
