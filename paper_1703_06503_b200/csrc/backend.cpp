@@ -87,7 +87,7 @@ struct Plan {
     // SGEMM TAILK: 1-D grid of whole tiles + K-split tail tiles (ptxgen_gemm.cpp)
     bool tailk = false;
     bool sk = false;  // SGEMM stream-K (ptxgen_gemm SK)
-    unsigned tiles_x = 0, tiles_y = 0, ktiles = 0, tile_floats = 0;
+    unsigned tiles_x = 0, tiles_y = 0, ktiles = 0, tile_floats = 0, ktile_k = 0;
 };
 
 // Relative NVRTC cost of a kernel whose fully unrolled body holds `n` FMAs
@@ -830,13 +830,15 @@ bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
     // split keeps K/s >= 4096) and at most 16 tiles per SM -- or when a
     // split count is forced (KTC_GEMM_SPLIT, tests and probes).
     const long long tiles = (I.M / MWG) * (I.N / NWG);
-    // Stream-K (SK) where whole tiles land unevenly on the SMs: the busiest
-    // SM runs ceil(c) tiles for c = tiles / SMs on average; below 92% balance
-    // (and with at least 8 K-tiles to deal) the units are dealt evenly.
+    // Stream-K (SK) where whole tiles leave the GPU under-filled: fewer than
+    // two tiles per SM on average and K >= 2048 (tools/sk_probe.py: 8192 x
+    // 256 x 8192 with 128x128 tiles 48.5 -> 57.1 TFLOP/s, 2048^3 128x128
+    // 51.6 -> 54.0; with 3.5 tiles per SM, or K = 1024, dealing K-ranges
+    // measured slower).  The launch keeps whole tiles when a CTA's share of
+    // K would be under 1024.
     const double per_sm = double(tiles) / double(std::max(be->ctx->limits.sm_count, 1));
     const bool sk = gemm_sk_policy() && gemm_source().ptx_generator && !std::getenv("KTC_GEMM_SPLIT") &&
-                    I.K / KWG >= 8 && tiles <= 16LL * be->ctx->limits.sm_count &&
-                    per_sm / std::ceil(per_sm) < 0.92;
+                    I.K >= 2048 && per_sm < 2.0;
     if (sk) {
         p->config.push_back(define("SK", 1));
         p->sk = true;
@@ -851,6 +853,7 @@ bool plan_gemm(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why)
         p->tiles_x = unsigned(I.M / MWG);
         p->tiles_y = unsigned(I.N / NWG);
         p->ktiles = unsigned(I.K / KWG);
+        p->ktile_k = unsigned(KWG);
         p->tile_floats = unsigned(MWG * NWG);
     }
     p->compile_cost = unrolled_cost(double((MWG / MDIMC) * (NWG / NDIMC) * KWI) + 64.0);
@@ -1139,8 +1142,10 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
                                                           size_t(plan.smem));
             const unsigned tiles = plan.tiles_x * plan.tiles_y;
             const unsigned long long U = (unsigned long long)tiles * plan.ktiles;
-            const unsigned G = unsigned(std::min<unsigned long long>(
+            unsigned G = unsigned(std::min<unsigned long long>(
                 U, (unsigned long long)std::max(occ, 1) * unsigned(ctx->limits.sm_count)));
+            // a CTA's share of K under 1024 -> one whole tile per CTA
+            if (U / G * plan.ktile_k < 1024) G = tiles;
             auto cv = [&](unsigned long long v) { return ((v + 1) * G - 1) / U; };
             unsigned maxseg = 1;
             for (unsigned t = 0; t < tiles; ++t)

@@ -341,10 +341,12 @@ def test_gemm_stream_k_matches_oracle(backend):
     launches (counters reset) -- all match the oracle."""
     names = "MWG NWG KWG MDIMC NDIMC SA SB MDIMA NDIMB STRM STRN VWM VWN KWI".split()
     rows = [(64, 64, 32, 16, 16, 1, 1, 16, 16, 0, 1, 4, 4, 8),
-            (64, 128, 16, 8, 8, 1, 1, 8, 16, 1, 1, 4, 8, 8),
-            (32, 32, 32, 8, 8, 0, 1, 8, 8, 0, 1, 2, 2, 2)]
-    for (m, n, k, a, b) in [(512, 512, 1024, 1.0, 0.0), (2048, 1280, 1024, 1.5, 0.5),
-                            (1024, 2048, 2048, 1.0, 0.0)]:
+            (128, 128, 32, 16, 16, 1, 1, 16, 16, 0, 1, 4, 4, 8),
+            (64, 128, 16, 8, 8, 1, 1, 8, 16, 1, 1, 4, 8, 8)]
+    # fewer than 2 tiles per SM and K >= 2048 -> stream-K (a CTA's share of
+    # K >= 1024, or whole tiles per CTA, both paths covered)
+    for (m, n, k, a, b) in [(1024, 512, 8192, 1.0, 0.0), (2048, 1024, 4096, 1.5, 0.5),
+                            (512, 256, 2048, 1.0, 0.0)]:
         want = O.gemm_reference(m, n, k, a, b)
         for row in rows:
             cfg = dict(zip(names, row))

@@ -295,3 +295,28 @@ def test_tf32_space_counts_follow_the_local_memory_expression():
     valid = {t.space_config(i) for i in range(want)}
     assert "BK=32;BN=256;CG=2;STAGES=6" in valid  # 6 x 32 KiB stages per CTA of a pair
     assert "BK=32;BN=256;CG=1;STAGES=6" not in valid
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_full_search_4096_replays_to_the_same_best_index(tmp_path):
+    """configs[4]: the measured times of the whole 852,608-configuration
+    SGEMM space at 4096^3 (profiles/fullsearch_4096, six GPU ranges of the
+    enumeration order) merged with the executor's rule give the same best
+    index and time as the reference's own run_full replaying them on its
+    ReplayBackend (backend.hpp:485-592)."""
+    import numpy as np
+
+    root = Path(__file__).resolve().parent.parent
+    times = np.load(root / "profiles" / "fullsearch_4096" / "gemm4096_times.npz")["times"]
+    t = pkg.Tuner.gemm(4096, 4096, 4096)
+    assert t.space_counts()[2] == len(times) == 852608 and np.isfinite(times).all()
+    best = int(np.argmin(times))  # first minimum = earliest index
+    with open(tmp_path / "measured.csv", "w") as f:
+        f.write("config,time_ms\n")
+        for i in range(len(times)):
+            f.write(f"{t.space_config(i)},{float(times[i])!r}\n")
+    job = {"template": "gemm", "problem": {"m": 4096, "n": 4096, "k": 4096}, "device": B200,
+           "strategy": {"kind": "full"}, "verify": False,
+           "backend": {"kind": "replay", "path": "measured.csv"}}
+    bi, bt = O.ref_job_run(json.dumps(job), str(tmp_path), str(tmp_path / "ref.csv"))
+    assert (bi, bt) == (best, float(times[best])) == (442805, float(times[442805]))
