@@ -36,6 +36,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--per-tile", type=int, default=8)
     ap.add_argument("--shapes", default="2048x2048x2048")
+    ap.add_argument("--variants", default="0:KTC_GEMM_SK=0;1:KTC_GEMM_SK=1",
+                    help='"name:ENV=V,ENV2=V;name2:..." (default: stream-K off / on)')
     ap.add_argument("--child", nargs=2)
     a = ap.parse_args()
     if a.child:
@@ -60,8 +62,12 @@ def main():
     for shape in a.shapes.split(","):
         m, n, k = (int(v) for v in shape.split("x"))
         res = {}
-        for mode in ("0", "1"):
-            env = dict(os.environ, KTC_GEMM_SK=mode)
+        variants = {}
+        for item in a.variants.split(";"):
+            name, _, envs = item.partition(":")
+            variants[name] = dict(kv.split("=", 1) for kv in envs.split(",") if kv)
+        for mode, extra in variants.items():
+            env = dict(os.environ, **extra)
             p = subprocess.run([sys.executable, __file__, "--child", shape, json.dumps(idx)], env=env,
                                capture_output=True, text=True, timeout=1800)
             res[mode] = json.loads(p.stdout.strip().splitlines()[-1]) if p.returncode == 0 else p.stderr[-800:]
