@@ -87,7 +87,7 @@ struct Plan {
     // SGEMM TAILK: 1-D grid of whole tiles + K-split tail tiles (ptxgen_gemm.cpp)
     bool tailk = false;
     bool sk = false;  // SGEMM stream-K (ptxgen_gemm SK)
-    unsigned tiles_x = 0, tiles_y = 0, ktiles = 0, tile_floats = 0, ktile_k = 0;
+    unsigned tiles_x = 0, tiles_y = 0, ktiles = 0, tile_floats = 0, ktile_k = 0, cg = 1;
 };
 
 // Relative NVRTC cost of a kernel whose fully unrolled body holds `n` FMAs
@@ -917,6 +917,15 @@ bool plan_custom(ktc_backend* be, const ktc_request* r, Plan* p, std::string* wh
 
 
 
+// TF32 stream-K (gemm_tf32.cu SK); KTC_TF32_SK=0 disables it.
+int tf32_sk_policy() {
+    static const int v = [] {
+        const char* e = std::getenv("KTC_TF32_SK");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 // TF32 tcgen05 variant (kernels/gemm_tf32.cu): one 128-thread CTA per
 // 128 x BN tile, TMA tensor maps for A (M-major) and B (N-major), SWIZZLE_128B.
 bool plan_gemm_tf32(ktc_backend* be, const ktc_request* r, Plan* p, std::string* why) {
@@ -940,15 +949,33 @@ bool plan_gemm_tf32(ktc_backend* be, const ktc_request* r, Plan* p, std::string*
         return false;
     }
     p->ksrc = &tf32_source();
-    p->config = {define("BN", BN), define("BK", BK), define("STAGES", STAGES), define("CG", CG)};
+    // Stream-K (SK host switch) for long-K problems whose (pair-)tiles fill
+    // less than one wave of one CTA per SM: the tiles x K-blocks units are
+    // dealt to the resident clusters (1024 x 1024 x 8192: 86 -> 63 us with
+    // 256 x 256 pair tiles).  With K = 2048 the partial-tile reductions cost
+    // more than the idle SMs (2048^3: 32.7 -> 50 us), so it stays off there.
+    const long long tiles = (I.M / (128 * CG)) * (I.N / BN);
+    const bool sk = tf32_sk_policy() && I.K >= 4096 && I.K / BK >= 8 &&
+                    tiles * CG < (long long)be->ctx->limits.sm_count;
+    p->config = {define("BN", BN), define("BK", BK), define("STAGES", STAGES), define("CG", CG),
+                 define("SK", sk ? 1 : 0)};
     p->smem = unsigned(STAGES * 4 * BK * (128 + BN / CG) + 2048);
     if (p->smem > be->ctx->limits.smem_per_block_optin) {
         *why = "needs " + std::to_string(p->smem) + " bytes of shared memory";
         return false;
     }
-    p->block[0] = 128;
+    p->block[0] = sk ? 192 : 128;
     p->grid[0] = unsigned(I.M / 128);
     p->grid[1] = unsigned(I.N / BN);
+    if (sk) {
+        p->sk = true;
+        p->tiles_x = unsigned(I.M / (128 * CG));  // tile rows (pairs for CG = 2)
+        p->tiles_y = unsigned(I.N / BN);
+        p->ktiles = unsigned(I.K / BK);
+        p->ktile_k = unsigned(BK);
+        p->tile_floats = unsigned(128 * BN);
+        p->cg = unsigned(CG);
+    }
     p->tma_mode = 2;
     p->box[0] = 32;
     p->box[1] = unsigned(BK);
@@ -1142,8 +1169,9 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
                                                           size_t(plan.smem));
             const unsigned tiles = plan.tiles_x * plan.tiles_y;
             const unsigned long long U = (unsigned long long)tiles * plan.ktiles;
+            // G = resident CTAs (SGEMM) or resident clusters of cg CTAs (TF32)
             unsigned G = unsigned(std::min<unsigned long long>(
-                U, (unsigned long long)std::max(occ, 1) * unsigned(ctx->limits.sm_count)));
+                U, (unsigned long long)std::max(occ, 1) * unsigned(ctx->limits.sm_count) / plan.cg));
             // a CTA's share of K under 1024 -> one whole tile per CTA
             if (U / G * plan.ktile_k < 1024) G = tiles;
             auto cv = [&](unsigned long long v) { return ((v + 1) * G - 1) / U; };
@@ -1151,8 +1179,9 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
             for (unsigned t = 0; t < tiles; ++t)
                 maxseg = std::max(maxseg, unsigned(cv((unsigned long long)(t + 1) * plan.ktiles - 1) -
                                                    cv((unsigned long long)t * plan.ktiles) + 1));
-            const size_t ws = size_t(tiles) * maxseg * plan.tile_floats * 4;
-            const size_t cn = size_t(tiles) * 4;
+            // TF32: one partial / counter per CTA of a pair (its 128 rows)
+            const size_t ws = size_t(tiles) * plan.cg * maxseg * plan.tile_floats * 4;
+            const size_t cn = size_t(tiles) * plan.cg * 4;
             if (ws > be->tail_ws_bytes) {
                 if (be->tail_ws) d.cuMemFree(be->tail_ws);
                 be->tail_ws = 0;
@@ -1180,8 +1209,13 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
             tk_splits = maxseg;
             tk_gx = plan.tiles_x;
             tk_kt = plan.ktiles;
+            if (fam == FAM_GEMM_TF32) {
+                // gemm_tf32.cu SK: (..., tmap_a, tmap_b, W, cnt, U, MAXSEG, tile rows, K-blocks)
+                params.insert(params.end(), {&tmap, &tmap2});
+                plan.tma_mode = 0;  // tensor maps already passed
+            }
             params.insert(params.end(), {&tk_ws, &tk_cnt, &tk_full, &tk_splits, &tk_gx, &tk_kt});
-            plan.grid[0] = G;
+            plan.grid[0] = G * plan.cg;
             plan.grid[1] = 1;
         }
         if (plan.tailk) {

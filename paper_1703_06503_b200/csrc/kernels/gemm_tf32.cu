@@ -122,6 +122,36 @@ __device__ __forceinline__ void umma_commit_pair(u32 bar) {
         : "memory");
 }
 
+// Stream-K helpers.
+__device__ __forceinline__ void tmem_ld32(u32 taddr, u32 (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+          "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Arrive on an mbarrier of any CTA of the cluster (shared::cluster address).
+__device__ __forceinline__ void mbar_arrive_cluster(u32 bar_cluster) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_local(u32 bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void named_sync(u32 id, u32 n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 // UMMA shared-memory descriptor for MN-major 32-bit operands (sm_100): the
 // only layout UMMA accepts for MN-major TF32 is SWIZZLE_128B_BASE32B
 // (128-byte MN rows, 32-byte swizzle atoms over 4-row K groups), which is
@@ -176,6 +206,7 @@ __device__ __forceinline__ void umma_commit(u32 bar) {
 #define STAGE_BYTES (A_STAGE_BYTES + B_STAGE_BYTES)
 #define TMEM_COLS (BN < 32 ? 32 : BN)
 
+#if !SK
 extern "C" __global__ void __launch_bounds__(NT, 1)
 #if CG == 2
 __cluster_dims__(2, 1, 1)
@@ -372,6 +403,277 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
     }
 #endif
 }
+#else
+// ---- SK (host switch): stream-K over persistent CTAs / CTA pairs.  The
+// pair-tiles x K-blocks units are dealt as contiguous ranges [c*U/G,
+// (c+1)*U/G) to the G resident clusters; a cluster walks its range as
+// segments (one per tile it touches).  Warp 0 produces (TMA), warp 1 of the
+// leader issues the MMAs, warps 2-5 are the epilogue (TMEM lane quarter =
+// warp % 4).  A whole-tile segment stores the output; a partial one stores
+// its 128 x BN partial in workspace slot ((tile*CG + rank)*MAXSEG + j), and
+// the last segment of the tile to arrive (counter) sums the partials in
+// segment order (its own re-read from TMEM: deterministic) and stores the
+// output.  TMEM is handed back to the MMA warp through tmem_empty.
+#define NTH 192
+extern "C" __global__ void __launch_bounds__(NTH, 1)
+#if CG == 2
+__cluster_dims__(2, 1, 1)
+#endif
+KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float beta,
+          const float* __restrict__ A, const float* __restrict__ B,
+          const float* __restrict__ Cin, float* __restrict__ Cout,
+          const __grid_constant__ TensorMap tmap_a, const __grid_constant__ TensorMap tmap_b,
+          float* __restrict__ W, unsigned* __restrict__ cnt, const unsigned U,
+          const unsigned maxseg, const unsigned ntm, const unsigned KB) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<u64>(smem_raw) + 1023) & ~u64(1023));
+    // full[S], empty[S], acc, tmem_empty
+    u64* bars = reinterpret_cast<u64*>(smem + STAGES * STAGE_BYTES);
+    u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * STAGES + 2);
+    volatile u32* flag = tmem_slot + 1;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const u32 rank = CG == 2 ? cluster_rank() : 0u;
+    const unsigned c = blockIdx.x / CG, G = gridDim.x / CG;
+    const unsigned u0 = (unsigned)((unsigned long long)c * U / G);
+    const unsigned u1 = (unsigned)((unsigned long long)(c + 1) * U / G);
+    const u32 full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES),
+              accb = smem_u32(bars + 2 * STAGES), tempty = smem_u32(bars + 2 * STAGES + 1);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, 1);
+        }
+        mbar_init(accb, 1);
+        mbar_init(tempty, CG);  // one arrival per CTA's epilogue group
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<u64>(&tmap_a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<u64>(&tmap_b)) : "memory");
+    }
+    if (warp == 1) {
+#if CG == 2
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"((u32)TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+#else
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"((u32)TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+#endif
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+#if CG == 2
+    cluster_sync_all();
+#else
+    __syncthreads();
+#endif
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const u32 tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---- TMA producer: the cluster's units in order (runs ahead across segments)
+        unsigned it = 0;
+        for (unsigned u = u0; u < u1; ++u, ++it) {
+            if (lane == 0) {
+                const unsigned t = u / KB, kb = u - t * KB;
+                const unsigned mp = t % ntm, np = t / ntm;
+                const int m0 = (int)((mp * CG + rank) * BM), n0 = (int)(np * BN);
+                const int s = (int)(it % STAGES);
+                const u32 phase = (it / STAGES) & 1u;
+                mbar_wait(empty0 + 8 * s, phase ^ 1u);
+                const u32 full = full0 + 8 * s;
+                if (rank == 0) mbar_expect_tx(full, CG * STAGE_BYTES);
+                const u32 sa = smem_u32(smem + s * STAGE_BYTES);
+                const u32 sb = sa + A_STAGE_BYTES;
+#if CG == 2
+                const u32 fullc = mapa_rank(full, 0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    tma_load_2d_pair(sa + j * A_BOX_BYTES, &tmap_a, fullc, m0 + 32 * j, (int)kb * BK);
+#pragma unroll
+                for (int j = 0; j < BNL / 32; ++j)
+                    tma_load_2d_pair(sb + j * A_BOX_BYTES, &tmap_b, fullc,
+                                     n0 + (int)rank * BNL + 32 * j, (int)kb * BK);
+#else
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    tma_load_2d(sa + j * A_BOX_BYTES, &tmap_a, full, m0 + 32 * j, (int)kb * BK);
+#pragma unroll
+                for (int j = 0; j < BN / 32; ++j)
+                    tma_load_2d(sb + j * A_BOX_BYTES, &tmap_b, full, n0 + 32 * j, (int)kb * BK);
+#endif
+            }
+            __syncwarp();
+        }
+    } else if (warp == 1) {
+        // ---- MMA issuer (leader CTA, one elected lane), one accumulator per segment
+        if (rank == 0) {
+            unsigned it = 0, seg = 0;
+            for (unsigned u = u0; u < u1; ++seg) {
+                const unsigned t = u / KB, kb0 = u - t * KB;
+                const unsigned kb1 = min(KB, kb0 + (u1 - u));
+                if (lane == 0) {
+                    if (seg > 0) mbar_wait(tempty, (seg - 1) & 1u);  // epilogue done with TMEM
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    for (unsigned kb = kb0; kb < kb1; ++kb, ++it) {
+                        const int s = (int)(it % STAGES);
+                        mbar_wait(full0 + 8 * s, (it / STAGES) & 1u);
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        const u32 sa = smem_u32(smem + s * STAGE_BYTES);
+                        const u32 sb = sa + A_STAGE_BYTES;
+#pragma unroll
+                        for (int kk = 0; kk < BK / 8; ++kk) {
+                            const u64 ad = umma_desc(sa + kk * 1024, A_BOX_BYTES, 512);
+                            const u64 bd = umma_desc(sb + kk * 1024, A_BOX_BYTES, 512);
+                            const u32 acc = (kb != kb0 || kk != 0) ? 1u : 0u;
+#if CG == 2
+                            umma_tf32_pair(tmem, ad, bd, make_idesc(256, BN), acc);
+#else
+                            umma_tf32(tmem, ad, bd, make_idesc(128, BN), acc);
+#endif
+                        }
+#if CG == 2
+                        umma_commit_pair(empty0 + 8 * s);
+#else
+                        umma_commit(empty0 + 8 * s);
+#endif
+                    }
+#if CG == 2
+                    umma_commit_pair(accb);
+#else
+                    umma_commit(accb);
+#endif
+                } else {
+                    it += kb1 - kb0;
+                }
+                __syncwarp();
+                u += kb1 - kb0;
+            }
+        }
+    } else {
+        // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4 (hardware rule)
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const bool lead = (warp == 2 && lane == 0);
+        const u32 tempty_leader = CG == 2 ? mapa_rank(tempty, 0) : tempty;
+        unsigned seg = 0;
+        for (unsigned u = u0; u < u1; ++seg) {
+            const unsigned t = u / KB, kb0 = u - t * KB;
+            const unsigned kb1 = min(KB, kb0 + (u1 - u));
+            const unsigned mp = t % ntm, np = t / ntm;
+            const int m0 = (int)((mp * CG + rank) * BM), n0 = (int)(np * BN);
+            // segments of tile t: the clusters holding its first and last unit
+            const unsigned first = (unsigned)(((unsigned long long)(t * KB + 1) * G - 1) / U);
+            const unsigned last = (unsigned)(((unsigned long long)((t + 1) * KB) * G - 1) / U);
+            const unsigned nseg = last - first + 1, j = c - first;
+            mbar_wait(accb, seg & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const u32 trow = tmem + ((u32)(q * 32) << 16);
+            float* crow = Cout + (size_t)(m0 + row) * N + n0;
+            const float* cin = Cin + (size_t)(m0 + row) * N + n0;
+            bool final_tile = nseg == 1;
+            float* wbase = W + (size_t)(t * CG + rank) * maxseg * (size_t)(BM * BN);
+            if (!final_tile) {
+                // Partials column-major within the tile (element (row, col) at
+                // col * BM + row): the 32 lanes of a warp hold 32 consecutive
+                // rows, so every store / load below is one 128-byte line.
+                float* wmine = wbase + (size_t)j * (BM * BN) + row;
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    u32 v[32];
+                    tmem_ld32(trow + (u32)c0, v);
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        __stcg(wmine + (size_t)(c0 + e) * BM, __uint_as_float(v[e]));
+                }
+                // publish: the group's stores are ordered before the lead's
+                // release fence by the barrier (cumulativity), then count
+                named_sync(1, 128);
+                if (lead) {
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    *flag = atomicAdd(&cnt[t * CG + rank], 1u);
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                }
+                named_sync(1, 128);
+                final_tile = *flag == nseg - 1;
+                if (final_tile && lead) cnt[t * CG + rank] = 0u;  // ready for the next launch
+            }
+            if (final_tile) {
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    u32 v[32];
+                    tmem_ld32(trow + (u32)c0, v);
+                    float acc[32];
+                    if (nseg == 1) {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) acc[e] = __uint_as_float(v[e]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) acc[e] = 0.0f;
+                        for (unsigned i = 0; i < nseg; ++i) {
+                            if (i == j) {
+#pragma unroll
+                                for (int e = 0; e < 32; ++e) acc[e] += __uint_as_float(v[e]);
+                            } else {
+                                const float* wp = wbase + (size_t)i * (BM * BN) + row;
+#pragma unroll
+                                for (int e = 0; e < 32; ++e)
+                                    acc[e] += __ldcg(wp + (size_t)(c0 + e) * BM);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < 32; e += 4) {
+                        float4 o;
+                        o.x = alpha * acc[e];
+                        o.y = alpha * acc[e + 1];
+                        o.z = alpha * acc[e + 2];
+                        o.w = alpha * acc[e + 3];
+                        if (beta != 0.0f) {
+                            const float4 cc = __ldg(reinterpret_cast<const float4*>(cin + c0 + e));
+                            o.x += beta * cc.x;
+                            o.y += beta * cc.y;
+                            o.z += beta * cc.z;
+                            o.w += beta * cc.w;
+                        }
+                        *reinterpret_cast<float4*>(crow + c0 + e) = o;
+                    }
+                }
+            }
+            // hand TMEM back to the MMA warp (one arrival per CTA)
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            named_sync(1, 128);
+            if (lead) mbar_arrive_cluster(tempty_leader);
+            u += kb1 - kb0;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+#if CG == 2
+    cluster_sync_relaxed();
+#else
+    __syncthreads();
+#endif
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1) {
+#if CG == 2
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"((u32)TMEM_COLS)
+                     : "memory");
+#else
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"((u32)TMEM_COLS)
+                     : "memory");
+#endif
+    }
+}
+#undef NTH
+#endif
 #undef BM
 #undef NT
 #undef BNL

@@ -282,6 +282,24 @@ def test_gemm_tf32_tcgen05_configs(backend, m, n, k):
     assert seen >= 12
 
 
+def test_gemm_tf32_stream_k_matches_oracle(backend):
+    """TF32 stream-K (long K, fewer (pair-)tiles than SMs): the persistent
+    clusters' partial 128 x BN tiles meet in the workspace (column-major, one
+    line per warp access) and the last segment sums them in segment order;
+    CTA pairs and single CTAs, alpha/beta, repeated launches -- rel 1e-3
+    against the fp32 oracle."""
+    for (m, n, k, a, b) in [(1024, 1024, 8192, 1.0, 0.0), (1024, 768, 8192, 1.5, 0.5)]:
+        want = O.gemm_reference(m, n, k, a, b)
+        for cfg in (dict(BN=256, BK=64, STAGES=3, CG=2), dict(BN=128, BK=32, STAGES=4, CG=2),
+                    dict(BN=128, BK=64, STAGES=3, CG=1)):
+            if m % (128 * cfg["CG"]) or n % cfg["BN"]:
+                continue
+            r = backend.evaluate(pkg.gemm_request(m, n, k, cfg, alpha=a, beta=b, tf32=True, reps=3))
+            assert r.ok and r.verification == "pass", (m, n, k, cfg, r)
+            rep = O.verify(backend.read_output(m * n), want, 1e-3, 1e-6)
+            assert rep["pass"], (m, n, k, cfg, rep)
+
+
 def test_prune_factor_early_out_keeps_winner_and_verification(built):
     """prune_factor (ktc.h): slow configurations are timed once, still verified;
     the winner's time is unaffected (it is never pruned: its first launch is
