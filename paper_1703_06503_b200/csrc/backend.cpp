@@ -1062,7 +1062,7 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
     }
     ktc_fn* fn = &fn_storage;
 
-    alignas(64) CUtensorMap tmap, tmap2;
+    alignas(64) CUtensorMap tmap, tmap2, tmap3;
     std::memset(&tmap, 0, sizeof(tmap));
     std::memset(&tmap2, 0, sizeof(tmap2));
     std::vector<void*> params;
@@ -1145,6 +1145,20 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
             };
             CUresult rc = encode(&tmap, I.dev[5], I.M, I.K);
             if (rc == CUDA_SUCCESS) rc = encode(&tmap2, I.dev[6], I.N, I.K);
+            if (rc == CUDA_SUCCESS && !plan.sk) {
+                // output C (M x N, N contiguous) for the TMA-store epilogue:
+                // 32-column x 128-row boxes, 128-byte swizzle
+                cuuint64_t dims[2] = {cuuint64_t(I.N), cuuint64_t(I.M)};
+                cuuint64_t strides[1] = {cuuint64_t(I.N) * 4};
+                cuuint32_t box[2] = {32, 128};
+                cuuint32_t estr[2] = {1, 1};
+                rc = d.cuTensorMapEncodeTiled(&tmap3, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                              reinterpret_cast<void*>(I.out[0]), dims, strides, box,
+                                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                              CU_TENSOR_MAP_SWIZZLE_128B,
+                                              CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            }
             if (rc != CUDA_SUCCESS) {
                 set_msg(out, cu_error_text(rc, "cuTensorMapEncodeTiled"));
                 return KTC_OK;
@@ -1279,6 +1293,7 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
         if (plan.tma_mode == 2) {
             params.push_back(&tmap);
             params.push_back(&tmap2);
+            if (fam == FAM_GEMM_TF32) params.push_back(&tmap3);
         }
     } else {
         st = refresh_custom_buffers(be);

@@ -122,6 +122,16 @@ __device__ __forceinline__ void umma_commit_pair(u32 bar) {
         : "memory");
 }
 
+// TMA store of a staged smem box (bulk-group completion).
+__device__ __forceinline__ void tma_store_2d(const TensorMap* map, u32 src, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+            reinterpret_cast<u64>(map)),
+        "r"(src), "r"(x), "r"(y)
+        : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
 // Stream-K helpers.
 __device__ __forceinline__ void tmem_ld32(u32 taddr, u32 (&v)[32]) {
     asm volatile(
@@ -214,7 +224,8 @@ __cluster_dims__(2, 1, 1)
 KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float beta,
           const float* __restrict__ A, const float* __restrict__ B,
           const float* __restrict__ Cin, float* __restrict__ Cout,
-          const __grid_constant__ TensorMap tmap_a, const __grid_constant__ TensorMap tmap_b) {
+          const __grid_constant__ TensorMap tmap_a, const __grid_constant__ TensorMap tmap_b,
+          const __grid_constant__ TensorMap tmap_c) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for SWIZZLE_128B atoms (same offset in both CTAs
     // of a pair: the leader's MMA descriptors address the peer's operands).
@@ -350,24 +361,44 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
     mbar_wait(accb, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int row = warp * 32 + lane;  // TMEM lane == tile row
+    if (beta == 0.0f) {
+        // Stores through TMA: each 128-row x 32-column chunk is staged in the
+        // now idle operand ring (two 16 KB buffers, 128-byte swizzle so the
+        // row-per-thread writes are bank-conflict free) and written by one
+        // bulk tensor store of full lines, overlapping the next chunk's
+        // TMEM load.
+        const u32 stg = smem_u32(smem);
+        int buf = 0;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32, buf ^= 1) {
+            u32 v[32];
+            tmem_ld32(tmem + ((u32)(warp * 32) << 16) + (u32)c0, v);
+            if (threadIdx.x == 0 && c0 >= 64)
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buffer free
+            __syncthreads();
+            const u32 sb = stg + (u32)buf * 16384u + (u32)row * 128u;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const u32 dst = sb + (u32)((q ^ (row & 7)) << 4);
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst),
+                             "f"(alpha * __uint_as_float(v[4 * q])),
+                             "f"(alpha * __uint_as_float(v[4 * q + 1])),
+                             "f"(alpha * __uint_as_float(v[4 * q + 2])),
+                             "f"(alpha * __uint_as_float(v[4 * q + 3]))
+                             : "memory");
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (threadIdx.x == 0) tma_store_2d(&tmap_c, stg + (u32)buf * 16384u, n0 + c0, m0);
+        }
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    } else {
     float* crow = Cout + (size_t)(m0 + row) * N + n0;
     const float* cin = Cin + (size_t)(m0 + row) * N + n0;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
         u32 v[32];
-        const u32 taddr = tmem + ((u32)(warp * 32) << 16) + (u32)c0;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-              "=r"(v[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tmem_ld32(tmem + ((u32)(warp * 32) << 16) + (u32)c0, v);
 #pragma unroll
         for (int q = 0; q < 32; q += 4) {
             float4 o;
@@ -375,15 +406,14 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
             o.y = alpha * __uint_as_float(v[q + 1]);
             o.z = alpha * __uint_as_float(v[q + 2]);
             o.w = alpha * __uint_as_float(v[q + 3]);
-            if (beta != 0.0f) {
-                const float4 c = __ldg(reinterpret_cast<const float4*>(cin + c0 + q));
-                o.x += beta * c.x;
-                o.y += beta * c.y;
-                o.z += beta * c.z;
-                o.w += beta * c.w;
-            }
+            const float4 c = __ldg(reinterpret_cast<const float4*>(cin + c0 + q));
+            o.x += beta * c.x;
+            o.y += beta * c.y;
+            o.z += beta * c.z;
+            o.w += beta * c.w;
             *reinterpret_cast<float4*>(crow + c0 + q) = o;
         }
+    }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 #if CG == 2
