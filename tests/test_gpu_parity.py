@@ -282,6 +282,20 @@ def test_gemm_tf32_tcgen05_configs(backend, m, n, k):
     assert seen >= 12
 
 
+def test_gemm_tf32_epilogues_alpha_beta(backend):
+    """Both TF32 epilogues: beta == 0 goes through the TMA-store path (chunks
+    staged in the operand ring, bulk tensor stores), beta != 0 through the
+    register path that reads Cin -- each against the fp32 oracle (rel 1e-3)."""
+    m, n, k = 512, 512, 1024
+    for (a, b) in [(1.0, 0.0), (1.5, 0.0), (1.5, 0.5), (-0.5, 2.0)]:
+        want = O.gemm_reference(m, n, k, a, b)
+        for cfg in (dict(BN=256, BK=32, STAGES=3, CG=2), dict(BN=64, BK=64, STAGES=2, CG=1)):
+            r = backend.evaluate(pkg.gemm_request(m, n, k, cfg, alpha=a, beta=b, tf32=True, reps=2))
+            assert r.ok and r.verification == "pass", (a, b, cfg, r)
+            rep = O.verify(backend.read_output(m * n), want, 1e-3, 1e-6)
+            assert rep["pass"], (a, b, cfg, rep)
+
+
 def test_gemm_tf32_stream_k_matches_oracle(backend):
     """TF32 stream-K (long K, fewer (pair-)tiles than SMs): the persistent
     clusters' partial 128 x BN tiles meet in the workspace (column-major, one
