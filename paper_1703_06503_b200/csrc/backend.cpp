@@ -955,7 +955,7 @@ bool plan_gemm_tf32(ktc_backend* be, const ktc_request* r, Plan* p, std::string*
     // 256 x 256 pair tiles).  With K = 2048 the partial-tile reductions cost
     // more than the idle SMs (2048^3: 32.7 -> 50 us), so it stays off there.
     const long long tiles = (I.M / (128 * CG)) * (I.N / BN);
-    const bool sk = tf32_sk_policy() && I.K >= 4096 && I.K / BK >= 8 &&
+    const bool sk = tf32_sk_policy() && (I.K >= 4096 || tf32_sk_policy() == 2) && I.K / BK >= 8 &&
                     tiles * CG < (long long)be->ctx->limits.sm_count;
     p->config = {define("BN", BN), define("BK", BK), define("STAGES", STAGES), define("CG", CG),
                  define("SK", sk ? 1 : 0)};

@@ -458,9 +458,9 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<u64>(smem_raw) + 1023) & ~u64(1023));
-    // full[S], empty[S], acc, tmem_empty
+    // full[S], empty[S], acc, tmem_empty, partial-staging barrier
     u64* bars = reinterpret_cast<u64*>(smem + STAGES * STAGE_BYTES);
-    u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * STAGES + 2);
+    u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * STAGES + 3);
     volatile u32* flag = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -469,7 +469,8 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
     const unsigned u0 = (unsigned)((unsigned long long)c * U / G);
     const unsigned u1 = (unsigned)((unsigned long long)(c + 1) * U / G);
     const u32 full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES),
-              accb = smem_u32(bars + 2 * STAGES), tempty = smem_u32(bars + 2 * STAGES + 1);
+              accb = smem_u32(bars + 2 * STAGES), tempty = smem_u32(bars + 2 * STAGES + 1),
+              pbar = smem_u32(bars + 2 * STAGES + 2);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -478,6 +479,7 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
         }
         mbar_init(accb, 1);
         mbar_init(tempty, CG);  // one arrival per CTA's epilogue group
+        mbar_init(pbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<u64>(&tmap_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<u64>(&tmap_b)) : "memory");
@@ -592,7 +594,7 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
         const int row = q * 32 + lane;
         const bool lead = (warp == 2 && lane == 0);
         const u32 tempty_leader = CG == 2 ? mapa_rank(tempty, 0) : tempty;
-        unsigned seg = 0;
+        unsigned seg = 0, pphase = 0;
         for (unsigned u = u0; u < u1; ++seg) {
             const unsigned t = u / KB, kb0 = u - t * KB;
             const unsigned kb1 = min(KB, kb0 + (u1 - u));
@@ -634,7 +636,75 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
                 final_tile = *flag == nseg - 1;
                 if (final_tile && lead) cnt[t * CG + rank] = 0u;  // ready for the next launch
             }
-            if (final_tile) {
+            // The other segments' partials, half a tile at a time, staged by
+            // bulk copies into the operand ring -- free once this is the
+            // cluster's last segment (all its loads consumed) -- so the sum
+            // reads shared memory instead of latency-bound global loads.
+            constexpr unsigned HALF = BM * (BN / 2) * 4;
+            const bool staged = final_tile && nseg > 1 && u + (kb1 - kb0) >= u1 &&
+                                (nseg - 1) * HALF <= (unsigned)(STAGES * STAGE_BYTES);
+            if (staged) {
+                const u32 ring = smem_u32(smem);
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {
+                    if (lead) {
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                        mbar_expect_tx(pbar, (nseg - 1) * HALF);
+                        unsigned k = 0;
+                        for (unsigned i = 0; i < nseg; ++i) {
+                            if (i == j) continue;
+                            const float* src = wbase + (size_t)i * (BM * BN) + (size_t)h * (BM * (BN / 2));
+                            asm volatile(
+                                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+                                " [%0], [%1], %2, [%3];" ::"r"(ring + k * HALF),
+                                "l"(reinterpret_cast<u64>(src)), "r"(HALF), "r"(pbar)
+                                : "memory");
+                            ++k;
+                        }
+                    }
+                    mbar_wait(pbar, pphase);
+                    pphase ^= 1u;
+                    const float* sp = reinterpret_cast<const float*>(smem);
+#pragma unroll 1
+                    for (int c0 = h * (BN / 2); c0 < (h + 1) * (BN / 2); c0 += 32) {
+                        u32 v[32];
+                        tmem_ld32(trow + (u32)c0, v);
+                        float acc[32];
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) acc[e] = 0.0f;
+                        unsigned k = 0;
+                        for (unsigned i = 0; i < nseg; ++i) {
+                            if (i == j) {
+#pragma unroll
+                                for (int e = 0; e < 32; ++e) acc[e] += __uint_as_float(v[e]);
+                            } else {
+                                const float* q = sp + (size_t)k * (HALF / 4) +
+                                                 (size_t)(c0 - h * (BN / 2)) * BM + row;
+#pragma unroll
+                                for (int e = 0; e < 32; ++e) acc[e] += q[(size_t)e * BM];
+                                ++k;
+                            }
+                        }
+#pragma unroll
+                        for (int e = 0; e < 32; e += 4) {
+                            float4 o;
+                            o.x = alpha * acc[e];
+                            o.y = alpha * acc[e + 1];
+                            o.z = alpha * acc[e + 2];
+                            o.w = alpha * acc[e + 3];
+                            if (beta != 0.0f) {
+                                const float4 cc = __ldg(reinterpret_cast<const float4*>(cin + c0 + e));
+                                o.x += beta * cc.x;
+                                o.y += beta * cc.y;
+                                o.z += beta * cc.z;
+                                o.w += beta * cc.w;
+                            }
+                            *reinterpret_cast<float4*>(crow + c0 + e) = o;
+                        }
+                    }
+                    named_sync(1, 128);  // the ring is read before the next half lands
+                }
+            } else if (final_tile) {
 #pragma unroll 1
                 for (int c0 = 0; c0 < BN; c0 += 32) {
                     u32 v[32];
