@@ -959,6 +959,7 @@ bool plan_gemm_tf32(ktc_backend* be, const ktc_request* r, Plan* p, std::string*
                     tiles * CG < (long long)be->ctx->limits.sm_count;
     p->config = {define("BN", BN), define("BK", BK), define("STAGES", STAGES), define("CG", CG),
                  define("SK", sk ? 1 : 0)};
+    if (sk && std::getenv("KTC_TF32_SK_TRACE")) p->config.push_back(define("SKTRACE", 1));
     p->smem = unsigned(STAGES * 4 * BK * (128 + BN / CG) + 2048);
     if (p->smem > be->ctx->limits.smem_per_block_optin) {
         *why = "needs " + std::to_string(p->smem) + " bytes of shared memory";
@@ -1071,6 +1072,8 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
     float fW = 0, fA = 0, fB = 0;
     CUdeviceptr pImg = 0, pOut = 0, pA = 0, pB = 0, pC = 0;
     CUdeviceptr tk_ws = 0, tk_cnt = 0, trace_buf = 0;
+    size_t sk_trace_off = 0;
+    unsigned sk_trace_ctas = 0;
     unsigned tk_full = 0, tk_splits = 1, tk_gx = 1, tk_kt = 1;
     std::vector<long long> scal_i;  // custom scalars
     std::vector<float> scal_f;
@@ -1194,7 +1197,11 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
                 maxseg = std::max(maxseg, unsigned(cv((unsigned long long)(t + 1) * plan.ktiles - 1) -
                                                    cv((unsigned long long)t * plan.ktiles) + 1));
             // TF32: one partial / counter per CTA of a pair (its 128 rows)
-            const size_t ws = size_t(tiles) * plan.cg * maxseg * plan.tile_floats * 4;
+            // (+ a diagnostic timeline of 16 u64 per CTA when KTC_TF32_SK_TRACE is set)
+            const size_t ws_part = size_t(tiles) * plan.cg * maxseg * plan.tile_floats * 4;
+            const size_t ws = ws_part + size_t(G) * plan.cg * 128;
+            sk_trace_off = ws_part;
+            sk_trace_ctas = G * plan.cg;
             const size_t cn = size_t(tiles) * plan.cg * 4;
             if (ws > be->tail_ws_bytes) {
                 if (be->tail_ws) d.cuMemFree(be->tail_ws);
@@ -1349,6 +1356,20 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
     st = ktc_launch_timed_pruned(ctx, fn, plan.grid, plan.block, plan.smem, params.data(),
                                  be->opts.warmup, reps, be->opts.flush_l2, bar, &best, all.data(),
                                  &reps_done);
+    if (sk_trace_ctas && std::getenv("KTC_TF32_SK_TRACE") && fam == FAM_GEMM_TF32 && !st) {
+        // TF32 stream-K timeline of the last launch (diagnostic)
+        static std::atomic<int> sk_n{0};
+        std::vector<unsigned long long> host(size_t(sk_trace_ctas) * 16);
+        if (d.cuCtxSynchronize() == CUDA_SUCCESS &&
+            d.cuMemcpyDtoH(host.data(), be->tail_ws + sk_trace_off, host.size() * 8) == CUDA_SUCCESS) {
+            const std::string path = std::string(std::getenv("KTC_TF32_SK_TRACE")) + "/sk_trace_" +
+                                     std::to_string(sk_n++) + ".bin";
+            if (FILE* f = std::fopen(path.c_str(), "wb")) {
+                std::fwrite(host.data(), 8, host.size(), f);
+                std::fclose(f);
+            }
+        }
+    }
     if (trace_buf) {
         static std::atomic<int> trace_n{0};
         const size_t n = size_t(plan.grid[0]) * plan.grid[1];

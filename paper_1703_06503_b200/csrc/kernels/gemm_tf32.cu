@@ -148,6 +148,12 @@ __device__ __forceinline__ void tmem_ld32(u32 taddr, u32 (&v)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // Arrive on an mbarrier of any CTA of the cluster (shared::cluster address).
 __device__ __forceinline__ void mbar_arrive_cluster(u32 bar_cluster) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster)
@@ -466,6 +472,16 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const u32 rank = CG == 2 ? cluster_rank() : 0u;
     const unsigned c = blockIdx.x / CG, G = gridDim.x / CG;
+#if SKTRACE
+    // diagnostic timeline (KTC_TF32_SK_TRACE): 16 u64 per CTA after the partial slots
+    unsigned long long* dbg = reinterpret_cast<unsigned long long*>(
+                                  W + (size_t)(U / KB) * CG * maxseg * (BM * BN)) +
+                              (size_t)blockIdx.x * 16;
+    if (threadIdx.x == 0) dbg[0] = gtimer();
+#define SKT(i) dbg[i] = gtimer()
+#else
+#define SKT(i)
+#endif
     const unsigned u0 = (unsigned)((unsigned long long)c * U / G);
     const unsigned u1 = (unsigned)((unsigned long long)(c + 1) * U / G);
     const u32 full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES),
@@ -552,6 +568,7 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
                 const unsigned kb1 = min(KB, kb0 + (u1 - u));
                 if (lane == 0) {
                     if (seg > 0) mbar_wait(tempty, (seg - 1) & 1u);  // epilogue done with TMEM
+                    if (seg < 3) SKT(2 + seg * 4);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     for (unsigned kb = kb0; kb < kb1; ++kb, ++it) {
                         const int s = (int)(it % STAGES);
@@ -581,6 +598,7 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
 #else
                     umma_commit(accb);
 #endif
+                    if (seg < 3) SKT(3 + seg * 4);
                 } else {
                     it += kb1 - kb0;
                 }
@@ -605,6 +623,7 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
             const unsigned last = (unsigned)(((unsigned long long)((t + 1) * KB) * G - 1) / U);
             const unsigned nseg = last - first + 1, j = c - first;
             mbar_wait(accb, seg & 1u);
+            if (lead && seg < 3) SKT(4 + seg * 4);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const u32 trow = tmem + ((u32)(q * 32) << 16);
             float* crow = Cout + (size_t)(m0 + row) * N + n0;
@@ -750,6 +769,7 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             named_sync(1, 128);
             if (lead) mbar_arrive_cluster(tempty_leader);
+            if (lead && seg < 3) SKT(5 + seg * 4);
             u += kb1 - kb0;
         }
     }
@@ -771,7 +791,16 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
                      : "memory");
 #endif
     }
+#if SKTRACE
+    if (threadIdx.x == 0) {
+        dbg[14] = gtimer();
+        u32 sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        dbg[15] = sm;
+    }
+#endif
 }
+#undef SKT
 #undef NTH
 #endif
 #undef BM
