@@ -1148,7 +1148,7 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
             };
             CUresult rc = encode(&tmap, I.dev[5], I.M, I.K);
             if (rc == CUDA_SUCCESS) rc = encode(&tmap2, I.dev[6], I.N, I.K);
-            if (rc == CUDA_SUCCESS && !plan.sk) {
+            if (rc == CUDA_SUCCESS) {
                 // output C (M x N, N contiguous) for the TMA-store epilogue:
                 // 32-column x 128-row boxes, 128-byte swizzle
                 cuuint64_t dims[2] = {cuuint64_t(I.N), cuuint64_t(I.M)};
@@ -1231,8 +1231,8 @@ int evaluate(ktc_backend* be, const ktc_request* r, ktc_result* out) {
             tk_gx = plan.tiles_x;
             tk_kt = plan.ktiles;
             if (fam == FAM_GEMM_TF32) {
-                // gemm_tf32.cu SK: (..., tmap_a, tmap_b, W, cnt, U, MAXSEG, tile rows, K-blocks)
-                params.insert(params.end(), {&tmap, &tmap2});
+                // gemm_tf32.cu SK: (..., tmap_a, tmap_b, tmap_c, W, cnt, U, MAXSEG, tile rows, K-blocks)
+                params.insert(params.end(), {&tmap, &tmap2, &tmap3});
                 plan.tma_mode = 0;  // tensor maps already passed
             }
             params.insert(params.end(), {&tk_ws, &tk_cnt, &tk_full, &tk_splits, &tk_gx, &tk_kt});

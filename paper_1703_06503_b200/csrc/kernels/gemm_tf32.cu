@@ -459,14 +459,16 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
           const float* __restrict__ A, const float* __restrict__ B,
           const float* __restrict__ Cin, float* __restrict__ Cout,
           const __grid_constant__ TensorMap tmap_a, const __grid_constant__ TensorMap tmap_b,
-          float* __restrict__ W, unsigned* __restrict__ cnt, const unsigned U,
+          const __grid_constant__ TensorMap tmap_c, float* __restrict__ W, unsigned* __restrict__ cnt, const unsigned U,
           const unsigned maxseg, const unsigned ntm, const unsigned KB) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<u64>(smem_raw) + 1023) & ~u64(1023));
-    // full[S], empty[S], acc, tmem_empty, partial-staging barrier
+    // full[S], empty[S], acc[2], tmem_empty[2], partial-staging barrier: the
+    // accumulator is double-buffered in TMEM (2 x BN columns), so the MMAs of
+    // segment s+1 run while the epilogue drains segment s.
     u64* bars = reinterpret_cast<u64*>(smem + STAGES * STAGE_BYTES);
-    u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * STAGES + 3);
+    u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * STAGES + 5);
     volatile u32* flag = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -485,8 +487,8 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
     const unsigned u0 = (unsigned)((unsigned long long)c * U / G);
     const unsigned u1 = (unsigned)((unsigned long long)(c + 1) * U / G);
     const u32 full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES),
-              accb = smem_u32(bars + 2 * STAGES), tempty = smem_u32(bars + 2 * STAGES + 1),
-              pbar = smem_u32(bars + 2 * STAGES + 2);
+              accb = smem_u32(bars + 2 * STAGES), tempty = smem_u32(bars + 2 * STAGES + 2),
+              pbar = smem_u32(bars + 2 * STAGES + 4);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -494,7 +496,9 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
             mbar_init(empty0 + 8 * s, 1);
         }
         mbar_init(accb, 1);
+        mbar_init(accb + 8, 1);
         mbar_init(tempty, CG);  // one arrival per CTA's epilogue group
+        mbar_init(tempty + 8, CG);
         mbar_init(pbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<u64>(&tmap_a)) : "memory");
@@ -504,13 +508,13 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
 #if CG == 2
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
-                     "r"((u32)TMEM_COLS)
+                     "r"((u32)(2 * TMEM_COLS))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
 #else
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
-                     "r"((u32)TMEM_COLS)
+                     "r"((u32)(2 * TMEM_COLS))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
 #endif
@@ -566,8 +570,10 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
             for (unsigned u = u0; u < u1; ++seg) {
                 const unsigned t = u / KB, kb0 = u - t * KB;
                 const unsigned kb1 = min(KB, kb0 + (u1 - u));
+                const u32 buf = seg & 1u;
                 if (lane == 0) {
-                    if (seg > 0) mbar_wait(tempty, (seg - 1) & 1u);  // epilogue done with TMEM
+                    // TMEM buffer `buf` was last used by segment seg-2
+                    if (seg >= 2) mbar_wait(tempty + 8 * buf, ((seg >> 1) - 1) & 1u);
                     if (seg < 3) SKT(2 + seg * 4);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     for (unsigned kb = kb0; kb < kb1; ++kb, ++it) {
@@ -582,9 +588,9 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
                             const u64 bd = umma_desc(sb + kk * 1024, A_BOX_BYTES, 512);
                             const u32 acc = (kb != kb0 || kk != 0) ? 1u : 0u;
 #if CG == 2
-                            umma_tf32_pair(tmem, ad, bd, make_idesc(256, BN), acc);
+                            umma_tf32_pair(tmem + buf * BN, ad, bd, make_idesc(256, BN), acc);
 #else
-                            umma_tf32(tmem, ad, bd, make_idesc(128, BN), acc);
+                            umma_tf32(tmem + buf * BN, ad, bd, make_idesc(128, BN), acc);
 #endif
                         }
 #if CG == 2
@@ -594,9 +600,9 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
 #endif
                     }
 #if CG == 2
-                    umma_commit_pair(accb);
+                    umma_commit_pair(accb + 8 * buf);
 #else
-                    umma_commit(accb);
+                    umma_commit(accb + 8 * buf);
 #endif
                     if (seg < 3) SKT(3 + seg * 4);
                 } else {
@@ -612,6 +618,7 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
         const int row = q * 32 + lane;
         const bool lead = (warp == 2 && lane == 0);
         const u32 tempty_leader = CG == 2 ? mapa_rank(tempty, 0) : tempty;
+        int sbuf = 0;  // TMA-store staging buffer (output through the idle ring)
         unsigned seg = 0, pphase = 0;
         for (unsigned u = u0; u < u1; ++seg) {
             const unsigned t = u / KB, kb0 = u - t * KB;
@@ -622,10 +629,11 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
             const unsigned first = (unsigned)(((unsigned long long)(t * KB + 1) * G - 1) / U);
             const unsigned last = (unsigned)(((unsigned long long)((t + 1) * KB) * G - 1) / U);
             const unsigned nseg = last - first + 1, j = c - first;
-            mbar_wait(accb, seg & 1u);
+            const u32 buf = seg & 1u;
+            mbar_wait(accb + 8 * buf, (seg >> 1) & 1u);
             if (lead && seg < 3) SKT(4 + seg * 4);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const u32 trow = tmem + ((u32)(q * 32) << 16);
+            const u32 trow = tmem + ((u32)(q * 32) << 16) + buf * BN;
             float* crow = Cout + (size_t)(m0 + row) * N + n0;
             const float* cin = Cin + (size_t)(m0 + row) * N + n0;
             bool final_tile = nseg == 1;
@@ -660,8 +668,53 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
             // cluster's last segment (all its loads consumed) -- so the sum
             // reads shared memory instead of latency-bound global loads.
             constexpr unsigned HALF = BM * (BN / 2) * 4;
-            const bool staged = final_tile && nseg > 1 && u + (kb1 - kb0) >= u1 &&
+            const bool last_seg = u + (kb1 - kb0) >= u1;  // the operand ring is idle
+            const bool staged = final_tile && nseg > 1 && last_seg &&
                                 (nseg - 1) * HALF <= (unsigned)(STAGES * STAGE_BYTES);
+            // Output through TMA stores from the idle ring (as in the one-tile
+            // kernel) when beta == 0 and two 16 KB staging buffers fit after
+            // the staged partials.
+            const u32 stg_base = smem_u32(smem) + (staged ? (nseg - 1) * HALF : 0u);
+            const bool tma_out = final_tile && last_seg && beta == 0.0f &&
+                                 (staged ? (nseg - 1) * HALF : 0u) + 32768u <=
+                                     (unsigned)(STAGES * STAGE_BYTES);
+            // one 128 x 32 output chunk: registers -> swizzled staging -> bulk store
+            auto out_chunk = [&](int c0, const float (&acc)[32]) {
+                if (tma_out) {
+                    if (lead) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    named_sync(1, 128);
+                    const u32 sb = stg_base + (u32)sbuf * 16384u + (u32)row * 128u;
+#pragma unroll
+                    for (int qq = 0; qq < 8; ++qq) {
+                        const u32 dst = sb + (u32)((qq ^ (row & 7)) << 4);
+                        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst),
+                                     "f"(alpha * acc[4 * qq]), "f"(alpha * acc[4 * qq + 1]),
+                                     "f"(alpha * acc[4 * qq + 2]), "f"(alpha * acc[4 * qq + 3])
+                                     : "memory");
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    named_sync(1, 128);
+                    if (lead) tma_store_2d(&tmap_c, stg_base + (u32)sbuf * 16384u, n0 + c0, m0);
+                    sbuf ^= 1;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; e += 4) {
+                        float4 o;
+                        o.x = alpha * acc[e];
+                        o.y = alpha * acc[e + 1];
+                        o.z = alpha * acc[e + 2];
+                        o.w = alpha * acc[e + 3];
+                        if (beta != 0.0f) {
+                            const float4 cc = __ldg(reinterpret_cast<const float4*>(cin + c0 + e));
+                            o.x += beta * cc.x;
+                            o.y += beta * cc.y;
+                            o.z += beta * cc.z;
+                            o.w += beta * cc.w;
+                        }
+                        *reinterpret_cast<float4*>(crow + c0 + e) = o;
+                    }
+                }
+            };
             if (staged) {
                 const u32 ring = smem_u32(smem);
 #pragma unroll 1
@@ -704,22 +757,7 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
                                 ++k;
                             }
                         }
-#pragma unroll
-                        for (int e = 0; e < 32; e += 4) {
-                            float4 o;
-                            o.x = alpha * acc[e];
-                            o.y = alpha * acc[e + 1];
-                            o.z = alpha * acc[e + 2];
-                            o.w = alpha * acc[e + 3];
-                            if (beta != 0.0f) {
-                                const float4 cc = __ldg(reinterpret_cast<const float4*>(cin + c0 + e));
-                                o.x += beta * cc.x;
-                                o.y += beta * cc.y;
-                                o.z += beta * cc.z;
-                                o.w += beta * cc.w;
-                            }
-                            *reinterpret_cast<float4*>(crow + c0 + e) = o;
-                        }
+                        out_chunk(c0, acc);
                     }
                     named_sync(1, 128);  // the ring is read before the next half lands
                 }
@@ -747,32 +785,19 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
                             }
                         }
                     }
-#pragma unroll
-                    for (int e = 0; e < 32; e += 4) {
-                        float4 o;
-                        o.x = alpha * acc[e];
-                        o.y = alpha * acc[e + 1];
-                        o.z = alpha * acc[e + 2];
-                        o.w = alpha * acc[e + 3];
-                        if (beta != 0.0f) {
-                            const float4 cc = __ldg(reinterpret_cast<const float4*>(cin + c0 + e));
-                            o.x += beta * cc.x;
-                            o.y += beta * cc.y;
-                            o.z += beta * cc.z;
-                            o.w += beta * cc.w;
-                        }
-                        *reinterpret_cast<float4*>(crow + c0 + e) = o;
-                    }
+                    out_chunk(c0, acc);
                 }
             }
+            if (tma_out && lead) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             // hand TMEM back to the MMA warp (one arrival per CTA)
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             named_sync(1, 128);
-            if (lead) mbar_arrive_cluster(tempty_leader);
+            if (lead) mbar_arrive_cluster(tempty_leader + 8 * buf);
             if (lead && seg < 3) SKT(5 + seg * 4);
             u += kb1 - kb0;
         }
     }
+    if (warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 #if CG == 2
     cluster_sync_relaxed();
@@ -783,11 +808,11 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
     if (warp == 1) {
 #if CG == 2
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                     "r"((u32)TMEM_COLS)
+                     "r"((u32)(2 * TMEM_COLS))
                      : "memory");
 #else
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                     "r"((u32)TMEM_COLS)
+                     "r"((u32)(2 * TMEM_COLS))
                      : "memory");
 #endif
     }
