@@ -154,14 +154,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-__device__ __forceinline__ void tmem_ld64(u32 taddr, u32 (&v)[64]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]), "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]), "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]), "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
 // Arrive on an mbarrier of any CTA of the cluster (shared::cluster address).
 __device__ __forceinline__ void mbar_arrive_cluster(u32 bar_cluster) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster)
@@ -382,43 +374,28 @@ KTC_ENTRY(const int M, const int N, const int K, const float alpha, const float 
         // bulk tensor store of full lines, overlapping the next chunk's
         // TMEM load.
         const u32 stg = smem_u32(smem);
-        // 64-column chunks (one tcgen05.ld.x64, two 32-column boxes) when two
-        // 32 KB staging buffers fit in the ring, else 32-column chunks
-        constexpr bool WIDE = BN >= 64 && STAGES * STAGE_BYTES >= 65536;
-        constexpr int CW = WIDE ? 64 : 32;
-        constexpr u32 BUFB = WIDE ? 32768u : 16384u;
         int buf = 0;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += CW, buf ^= 1) {
-            u32 v[64];
-            if (WIDE) {
-                tmem_ld64(tmem + ((u32)(warp * 32) << 16) + (u32)c0, v);
-            } else {
-                u32 (&v32)[32] = *reinterpret_cast<u32(*)[32]>(v);
-                tmem_ld32(tmem + ((u32)(warp * 32) << 16) + (u32)c0, v32);
-            }
-            if (threadIdx.x == 0 && c0 >= 2 * CW)
-                asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(WIDE ? 2 : 1) : "memory");
+        for (int c0 = 0; c0 < BN; c0 += 32, buf ^= 1) {
+            u32 v[32];
+            tmem_ld32(tmem + ((u32)(warp * 32) << 16) + (u32)c0, v);
+            if (threadIdx.x == 0 && c0 >= 64)
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buffer free
             __syncthreads();
+            const u32 sb = stg + (u32)buf * 16384u + (u32)row * 128u;
 #pragma unroll
-            for (int h = 0; h < CW / 32; ++h) {
-                const u32 sb = stg + (u32)buf * BUFB + (u32)h * 16384u + (u32)row * 128u;
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const u32 dst = sb + (u32)((q ^ (row & 7)) << 4);
-                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst),
-                                 "f"(alpha * __uint_as_float(v[32 * h + 4 * q])),
-                                 "f"(alpha * __uint_as_float(v[32 * h + 4 * q + 1])),
-                                 "f"(alpha * __uint_as_float(v[32 * h + 4 * q + 2])),
-                                 "f"(alpha * __uint_as_float(v[32 * h + 4 * q + 3]))
-                                 : "memory");
-                }
+            for (int q = 0; q < 8; ++q) {
+                const u32 dst = sb + (u32)((q ^ (row & 7)) << 4);
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst),
+                             "f"(alpha * __uint_as_float(v[4 * q])),
+                             "f"(alpha * __uint_as_float(v[4 * q + 1])),
+                             "f"(alpha * __uint_as_float(v[4 * q + 2])),
+                             "f"(alpha * __uint_as_float(v[4 * q + 3]))
+                             : "memory");
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
-            if (threadIdx.x == 0)
-                for (int h = 0; h < CW / 32; ++h)
-                    tma_store_2d(&tmap_c, stg + (u32)buf * BUFB + (u32)h * 16384u, n0 + c0 + 32 * h, m0);
+            if (threadIdx.x == 0) tma_store_2d(&tmap_c, stg + (u32)buf * 16384u, n0 + c0, m0);
         }
         if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     } else {
