@@ -379,6 +379,9 @@ std::string emit_entry(const ConvGen& g, const std::string& name) {
 
     if (g.UNR == 1) {
         const bool paired = g.CF2 && g.YWPT % 2 == 0;
+        // .b64 register of row pair (2p, 2p+1), column c while packed ("" = unpacked)
+        std::vector<std::vector<std::string>> accp(size_t(g.YWPT / 2 + 1),
+                                                   std::vector<std::string>(size_t(g.XWPT)));
         for (int gi = 0; gi < NG; ++gi) {
             for (int rr = 0; rr < ROWS; ++rr) {
                 const std::string a = window_addr(gi, rr);
@@ -399,25 +402,51 @@ std::string emit_entry(const ConvGen& g, const std::string& name) {
                     }
                 };
                 if (paired) {
+                    // Row pairs live in .b64 registers while they take FFMA2s:
+                    // packed once after row j's leading edge tap row (jj = 0),
+                    // unpacked once before row j+1's trailing one (jj = FS-1),
+                    // and each window value is broadcast to a pair once per
+                    // input row -- the same FMA sequence per output as one
+                    // pack / fma / unpack per FFMA2, with a third of the PTX.
+                    std::vector<std::string> wb(static_cast<size_t>(WINP));
+                    auto bcast = [&](int k) -> const std::string& {
+                        std::string& r = wb[size_t(k)];
+                        if (r.empty()) {
+                            r = x.d();
+                            x.op("mov.b64 " + r + ", {" + w[size_t(k)] + ", " + w[size_t(k)] + "}");
+                        }
+                        return r;
+                    };
                     for (int j = 0; j < g.YWPT; j += 2) {
                         const int jj = rr - j;
                         if (jj >= 1 && jj < g.FS) {
+                            for (int e = 0; e < g.VW; ++e) {
+                                std::string& pr = accp[size_t(j / 2)][size_t(gi * g.VW + e)];
+                                if (pr.empty()) {
+                                    pr = x.d();
+                                    x.op("mov.b64 " + pr + ", {" + acc[size_t(j)][size_t(gi * g.VW + e)] +
+                                         ", " + acc[size_t(j + 1)][size_t(gi * g.VW + e)] + "}");
+                                }
+                            }
                             for (int i = 0; i < g.FS; ++i) {
                                 const std::string t2 = x.d();
                                 x.op("ld.const.b64 " + t2 + ", [c_tpair+" + imm((jj * g.FS + i) * 8) + "]");
                                 for (int e = 0; e < g.VW; ++e) {
-                                    const std::string& a0 = acc[size_t(j)][size_t(gi * g.VW + e)];
-                                    const std::string& a1 = acc[size_t(j + 1)][size_t(gi * g.VW + e)];
-                                    const std::string wv = x.d(), av = x.d(), dv = x.d();
-                                    x.op("mov.b64 " + wv + ", {" + w[size_t(e + i)] + ", " + w[size_t(e + i)] + "}");
-                                    x.op("mov.b64 " + av + ", {" + a0 + ", " + a1 + "}");
-                                    x.op("fma.rn.f32x2 " + dv + ", " + t2 + ", " + wv + ", " + av);
-                                    x.op("mov.b64 {" + a0 + ", " + a1 + "}, " + dv);
+                                    const std::string& pr = accp[size_t(j / 2)][size_t(gi * g.VW + e)];
+                                    x.op("fma.rn.f32x2 " + pr + ", " + t2 + ", " + bcast(e + i) + ", " + pr);
                                 }
                             }
                         } else if (jj == 0) {
                             scalar_row(j, 0);
                         } else if (jj == g.FS) {
+                            for (int e = 0; e < g.VW; ++e) {
+                                std::string& pr = accp[size_t(j / 2)][size_t(gi * g.VW + e)];
+                                if (!pr.empty()) {
+                                    x.op("mov.b64 {" + acc[size_t(j)][size_t(gi * g.VW + e)] + ", " +
+                                         acc[size_t(j + 1)][size_t(gi * g.VW + e)] + "}, " + pr);
+                                    pr.clear();
+                                }
+                            }
                             scalar_row(j + 1, g.FS - 1);
                         }
                     }
