@@ -166,6 +166,7 @@ class CompileService {
     std::vector<std::thread> workers_;
     int want_threads_ = 0;
     int batch_ = 8;
+    int ptx_batch_ = 1;  // configurations per program for the PTX-generator families
     std::string cache_dir_;
     double compile_ms_ = 0.0;
     size_t programs_ = 0;
