@@ -377,12 +377,8 @@ bool CompileService::take_program_locked(Batch* out) {
         take(oldest);
     } else {
         size_t big = 0;
-        static const bool fifo = [] {
-            const char* e = std::getenv("KTC_COMPILE_ORDER");
-            return e && std::string(e) == "fifo";
-        }();
         for (size_t i = 1; i < q.items.size(); ++i)
-            if (fifo ? q.items[i].born < q.items[big].born : q.items[i].cost > q.items[big].cost) big = i;
+            if (q.items[i].cost > q.items[big].cost) big = i;
         double total = q.items[big].cost;
         const double share = (queued_cost_ + total_inflight_) / double(std::max(1, want_threads_));
         // PTX-generator families: ptxas has no NVVM-style fixed cost to
